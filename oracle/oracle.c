@@ -1,0 +1,296 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct FP64 CPU oracle for the
+ * dispersion-correction hot path of arXiv 2508.04951 (Vickers, Mack,
+ * Osaretin, "Real-Time Doppler and Ionospheric Dispersion Correction
+ * Techniques for Arbitrary Waveforms Utilizing GPU Compute").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load or call this
+ * library.  The product path (paper_2508_04951_b200/, libdispcorr) shares no
+ * code, header, table or constant generator with this file and never calls it.
+ *
+ * Citations: "P:Lnnn" = line nnn of the paper text; equation numbers
+ * follow source order (Eq. 1 at P:L89 ... Eq. 16 at P:L285).  Readings of
+ * silent/ambiguous passages are the ones listed in DESIGN.md section
+ * "Readings of the paper" (R1..R12); each use below names its reading.
+ *
+ * Arithmetic: IEEE binary64 throughout, no fast-math, no reassociation beyond
+ * what the definitions state.  Complex numbers are interleaved (re, im) pairs.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_PI 3.14159265358979323846264338327950288
+
+/* CODATA 2018 exact / recommended values (SI).  P:L91 Eq. 1 names the
+ * symbols; the paper gives no numbers (reading R5). */
+static const double ORC_QE = 1.602176634e-19;    /* electron charge, C (exact) */
+static const double ORC_ME = 9.1093837015e-31;   /* electron mass, kg          */
+static const double ORC_EPS0 = 8.8541878128e-12; /* vacuum permittivity, F/m   */
+static const double ORC_C = 299792458.0;         /* speed of light, m/s (exact) */
+
+/* ---------------------------------------------------------------------------
+ * Physical model
+ * ------------------------------------------------------------------------- */
+
+/* K2 / E = q_e^2 / (8 pi^2 m_e eps0)   [m^3/s^2 per (el/m^2)]
+ * Eq. 1 and Appendix A Eq. 21. */
+double orc_k2_per_tec(void) {
+  return (ORC_QE * ORC_QE) / (8.0 * ORC_PI * ORC_PI * ORC_ME * ORC_EPS0);
+}
+
+double orc_speed_of_light(void) { return ORC_C; }
+
+/* One-way group delay tau(f) = K2 / (c f^2), Eq. 1. */
+double orc_group_delay(double f_hz, double tec) {
+  double k2 = orc_k2_per_tec() * tec;
+  return k2 / (ORC_C * f_hz * f_hz);
+}
+
+/* alpha = (1 + v/c) / (1 - v/c), v > 0 approaching.  Eq. 13 context. */
+double orc_alpha_from_velocity(double v_mps) {
+  return (1.0 + v_mps / ORC_C) / (1.0 - v_mps / ORC_C);
+}
+
+/* ---------------------------------------------------------------------------
+ * Discrete Fourier transform.  X_k = sum_t x_t exp(sign * i 2 pi k t / n).
+ * sign = -1 is the forward transform (numpy / textbook convention, reading R1).
+ * ------------------------------------------------------------------------- */
+
+/* Direct O(n^2) DFT, the definition written out.  The exponent k*t is reduced
+ * modulo n in exact integer arithmetic (exp is 2 pi-periodic in the angle), so
+ * the angle stays in [0, 2 pi). */
+void orc_dft(int64_t n, const double *x, double *X, int sign) {
+  for (int64_t k = 0; k < n; ++k) {
+    double re = 0.0, im = 0.0;
+    for (int64_t t = 0; t < n; ++t) {
+      int64_t kt = (int64_t)(((__int128)k * t) % n);
+      double ang = (double)sign * 2.0 * ORC_PI * (double)kt / (double)n;
+      double c = cos(ang), s = sin(ang);
+      double xr = x[2 * t], xi = x[2 * t + 1];
+      re += xr * c - xi * s;
+      im += xr * s + xi * c;
+    }
+    X[2 * k] = re;
+    X[2 * k + 1] = im;
+  }
+}
+
+/* Textbook iterative radix-2 decimation-in-time FFT, in place, n = 2^p.
+ * Bit-reversal permutation followed by log2(n) butterfly stages with twiddles
+ * exp(sign * i 2 pi j / len) from cos/sin.  Unnormalised. */
+void orc_fft(int64_t n, double *x, int sign) {
+  /* bit reversal */
+  for (int64_t i = 1, j = 0; i < n; ++i) {
+    int64_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      double tr = x[2 * i], ti = x[2 * i + 1];
+      x[2 * i] = x[2 * j];
+      x[2 * i + 1] = x[2 * j + 1];
+      x[2 * j] = tr;
+      x[2 * j + 1] = ti;
+    }
+  }
+  for (int64_t len = 2; len <= n; len <<= 1) {
+    int64_t half = len >> 1;
+    for (int64_t j = 0; j < half; ++j) {
+      double ang = (double)sign * 2.0 * ORC_PI * (double)j / (double)len;
+      double wr = cos(ang), wi = sin(ang);
+      for (int64_t s = 0; s < n; s += len) {
+        int64_t a = s + j, b = s + j + half;
+        double br = x[2 * b] * wr - x[2 * b + 1] * wi;
+        double bi = x[2 * b] * wi + x[2 * b + 1] * wr;
+        double ar = x[2 * a], ai = x[2 * a + 1];
+        x[2 * a] = ar + br;
+        x[2 * a + 1] = ai + bi;
+        x[2 * b] = ar - br;
+        x[2 * b + 1] = ai - bi;
+      }
+    }
+  }
+}
+
+/* ---------------------------------------------------------------------------
+ * Ionospheric correction, Eq. 15:
+ *   S_Tx = F^-1[ F(S_Rx) exp(-4 pi i K2 / (c f)) ]
+ * and the forward (distortion) model, Eq. 14, with the opposite
+ * sign.  Steps (SURVEY O-IONO):
+ *   1. X = DFT(x)                                    (forward, e^{-i}; R1)
+ *   2. f_k = fc + fs (k - n [k >= n/2]) / n          (bin -> absolute RF; R2)
+ *   3. nu_k = 2 K2 / (c f_k) cycles if f_k > 0 else 0 (two-way 2 tau f; R3, R4)
+ *   4. Y_k = X_k exp(dir * i 2 pi nu_k), dir = -1 correct (Eq. 15), +1 distort (Eq. 14)
+ *   5. y = (1/n) IDFT(Y)                             (R6)
+ * exp(i 2 pi nu) is evaluated as exp(i 2 pi (nu - nearbyint(nu))): the same
+ * number (period 1 in nu), with the subtraction exact in binary64.
+ * method: 0 = radix-2 FFT (n must be a power of two), 1 = direct DFT.
+ * ------------------------------------------------------------------------- */
+double orc_bin_frequency(int64_t k, int64_t n, double fs, double fc) {
+  int64_t kk = (k >= n / 2) ? k - n : k; /* Nyquist bin n/2 is negative (R2) */
+  return fc + fs * (double)kk / (double)n;
+}
+
+double orc_iono_phase_cycles(double f_hz, double tec) {
+  if (!(f_hz > 0.0)) return 0.0; /* unit multiplier at f <= 0 (R3) */
+  double k2 = orc_k2_per_tec() * tec;
+  return 2.0 * k2 / (ORC_C * f_hz); /* 2 tau(f) f = 2 K2 / (c f), Eq. 14 */
+}
+
+int orc_iono_dir(int64_t n, double fs, double fc, double tec, int dir, int method,
+                 const double *x, double *y) {
+  if (n < 1) return -1;
+  double *X = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+  if (!X) return -2;
+  if (method == 1) {
+    orc_dft(n, x, X, -1);
+  } else {
+    memcpy(X, x, sizeof(double) * 2 * (size_t)n);
+    orc_fft(n, X, -1);
+  }
+  for (int64_t k = 0; k < n; ++k) {
+    double f = orc_bin_frequency(k, n, fs, fc);
+    double nu = orc_iono_phase_cycles(f, tec);
+    double r = nu - nearbyint(nu);
+    double ang = (double)dir * 2.0 * ORC_PI * r;
+    double c = cos(ang), s = sin(ang);
+    double xr = X[2 * k], xi = X[2 * k + 1];
+    X[2 * k] = xr * c - xi * s;
+    X[2 * k + 1] = xr * s + xi * c;
+  }
+  if (method == 1) {
+    orc_dft(n, X, y, +1);
+  } else {
+    memcpy(y, X, sizeof(double) * 2 * (size_t)n);
+    orc_fft(n, y, +1);
+  }
+  for (int64_t t = 0; t < 2 * n; ++t) y[t] /= (double)n;
+  free(X);
+  return 0;
+}
+
+/* Correction (Eq. 15). */
+int orc_iono(int64_t n, double fs, double fc, double tec, int method, const double *x,
+             double *y) {
+  return orc_iono_dir(n, fs, fc, tec, -1, method, x, y);
+}
+
+/* ---------------------------------------------------------------------------
+ * Doppler time-dilation correction by windowed Whittaker-Shannon
+ * interpolation, Eq. 16 restricted to a window of W samples
+ * (Alg. 1, window P:L533).  Resampling onto t/alpha
+ * undoes S(alpha t) (Eq. 13; reading R8).  Steps (SURVEY O-DOPP):
+ *   beta = 1/alpha; for m in [0, n):
+ *     t = m beta; k_lo = floor(t - W/2) + 1               (window {k: -W/2 < k - t <= W/2}; R9)
+ *     acc = sum_{k=k_lo}^{k_lo+W-1} [0 <= k < n] x_k sinc(t - k)   (zero outside; R12)
+ *     y_m = acc exp(-i 2 pi fc (1 - beta) m / fs)            (carrier term; R10)
+ * sinc(d) = 1 at d = 0, 0 at nonzero integer d, sin(pi d)/(pi d) otherwise
+ * (normalised sinc, Eq. 16; rectangular window, reading R11).
+ * ------------------------------------------------------------------------- */
+double orc_sinc(double d) {
+  if (d == 0.0) return 1.0;
+  if (d == floor(d)) return 0.0;
+  return sin(ORC_PI * d) / (ORC_PI * d);
+}
+
+int orc_doppler(int64_t n, int W, double fs, double fc, double alpha, const double *x,
+                double *y) {
+  if (n < 1 || W < 1 || !(alpha > 0.0)) return -1;
+  double beta = 1.0 / alpha;
+  for (int64_t m = 0; m < n; ++m) {
+    double t = (double)m * beta;
+    int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W) + 1;
+    double re = 0.0, im = 0.0;
+    for (int64_t k = k_lo; k < k_lo + W; ++k) {
+      if (k < 0 || k >= n) continue;
+      double h = orc_sinc(t - (double)k);
+      re += x[2 * k] * h;
+      im += x[2 * k + 1] * h;
+    }
+    /* carrier rotation; cycles reduced mod 1 (period 1) before the angle */
+    double psi = fc * (1.0 - beta) * (double)m / fs;
+    double r = psi - nearbyint(psi);
+    double ang = -2.0 * ORC_PI * r;
+    double c = cos(ang), s = sin(ang);
+    y[2 * m] = re * c - im * s;
+    y[2 * m + 1] = re * s + im * c;
+  }
+  return 0;
+}
+
+/* Exact (unwindowed) Whittaker-Shannon sum over the whole record, Eq. 16,
+ * O(n^2).  Used only as a brute-force pin for orc_doppler. */
+int orc_doppler_exact(int64_t n, double fs, double fc, double alpha, const double *x,
+                      double *y) {
+  double beta = 1.0 / alpha;
+  for (int64_t m = 0; m < n; ++m) {
+    double t = (double)m * beta;
+    double re = 0.0, im = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      double h = orc_sinc(t - (double)k);
+      re += x[2 * k] * h;
+      im += x[2 * k + 1] * h;
+    }
+    double psi = fc * (1.0 - beta) * (double)m / fs;
+    double r = psi - nearbyint(psi);
+    double ang = -2.0 * ORC_PI * r;
+    double c = cos(ang), s = sin(ang);
+    y[2 * m] = re * c - im * s;
+    y[2 * m + 1] = re * s + im * c;
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Batched entry points on complex64 inputs (the GPU's input type),
+ * upcast exactly to binary64; pulses are independent and may be run
+ * on several host threads (nthreads <= 0: OpenMP default).  Output binary64.
+ * stage: 1 = iono, 2 = doppler, 3 = correct = doppler(iono(x)) with a binary64
+ * intermediate (reading R7: iono first).
+ * ------------------------------------------------------------------------- */
+int orc_run_batch(int stage, int64_t n, int64_t batch, double fs, double fc, int W,
+                  const double *tec, const double *alpha, const float *x, double *y,
+                  int nthreads, int method) {
+  int err = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : err)
+#endif
+  for (int64_t p = 0; p < batch; ++p) {
+    double *xin = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+    double *tmp = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+    if (!xin || !tmp) {
+      err |= 1;
+      free(xin);
+      free(tmp);
+      continue;
+    }
+    const float *xp = x + (size_t)p * 2 * (size_t)n;
+    for (int64_t i = 0; i < 2 * n; ++i) xin[i] = (double)xp[i];
+    double *yp = y + (size_t)p * 2 * (size_t)n;
+    if (stage == 1) {
+      err |= orc_iono(n, fs, fc, tec[p], method, xin, yp) != 0;
+    } else if (stage == 2) {
+      err |= orc_doppler(n, W, fs, fc, alpha[p], xin, yp) != 0;
+    } else {
+      err |= orc_iono(n, fs, fc, tec[p], method, xin, tmp) != 0;
+      err |= orc_doppler(n, W, fs, fc, alpha[p], tmp, yp) != 0;
+    }
+    free(xin);
+    free(tmp);
+  }
+  return err ? -1 : 0;
+}
+
+int orc_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

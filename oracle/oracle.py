@@ -1,0 +1,187 @@
+"""ctypes front end of the FP64 CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, ``__graft_entry__.smoke()`` and
+bench.py's ``cpu_baseline`` / ``--impl reference`` leg.  The product package
+(``paper_2508_04951_b200``) never imports this module and shares no code with it.
+
+Every function follows the paper step by step; see the citations in oracle.c
+(Eq. 15 P:L231-236 for the ionospheric correction, Eq. 16 P:L285-288 with the
+window of P:L533 for the Doppler resampler) and the readings R1..R12 in
+DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with plain -O2 (no fast-math) into liboracle.so."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-fno-fast-math",
+               "-ffp-contract=off", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        d, i64, i32 = ctypes.c_double, ctypes.c_int64, ctypes.c_int
+        p = ctypes.c_void_p
+        lib.orc_k2_per_tec.restype = d
+        lib.orc_speed_of_light.restype = d
+        lib.orc_group_delay.restype = d
+        lib.orc_group_delay.argtypes = [d, d]
+        lib.orc_alpha_from_velocity.restype = d
+        lib.orc_alpha_from_velocity.argtypes = [d]
+        lib.orc_dft.argtypes = [i64, p, p, i32]
+        lib.orc_fft.argtypes = [i64, p, i32]
+        lib.orc_bin_frequency.restype = d
+        lib.orc_bin_frequency.argtypes = [i64, i64, d, d]
+        lib.orc_iono_phase_cycles.restype = d
+        lib.orc_iono_phase_cycles.argtypes = [d, d]
+        lib.orc_iono_dir.restype = i32
+        lib.orc_iono_dir.argtypes = [i64, d, d, d, i32, i32, p, p]
+        lib.orc_sinc.restype = d
+        lib.orc_sinc.argtypes = [d]
+        lib.orc_doppler.restype = i32
+        lib.orc_doppler.argtypes = [i64, i32, d, d, d, p, p]
+        lib.orc_doppler_exact.restype = i32
+        lib.orc_doppler_exact.argtypes = [i64, d, d, d, p, p]
+        lib.orc_run_batch.restype = i32
+        lib.orc_run_batch.argtypes = [i32, i64, i64, d, d, i32, p, p, p, p, i32, i32]
+        lib.orc_max_threads.restype = i32
+        _lib = lib
+    return _lib
+
+
+def _c128(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------------------- constants
+def k2_per_tec() -> float:
+    """K2/E = q_e^2/(8 pi^2 m_e eps0), Eq. 1, CODATA 2018."""
+    return _load().orc_k2_per_tec()
+
+
+def speed_of_light() -> float:
+    return _load().orc_speed_of_light()
+
+
+def group_delay(f_hz: float, tec: float) -> float:
+    """One-way tau(f) = K2/(c f^2), Eq. 1."""
+    return _load().orc_group_delay(f_hz, tec)
+
+
+def alpha_from_velocity(v_mps: float) -> float:
+    """alpha = (1+v/c)/(1-v/c)."""
+    return _load().orc_alpha_from_velocity(v_mps)
+
+
+def bin_frequency(k: int, n: int, fs: float, fc: float) -> float:
+    return _load().orc_bin_frequency(k, n, fs, fc)
+
+
+def iono_phase_cycles(f_hz: float, tec: float) -> float:
+    """nu = 2 K2/(c f) cycles (0 for f <= 0)."""
+    return _load().orc_iono_phase_cycles(f_hz, tec)
+
+
+def sinc(d: float) -> float:
+    return _load().orc_sinc(d)
+
+
+# ----------------------------------------------------------------------------- transforms
+def dft(x, sign: int = -1) -> np.ndarray:
+    x = _c128(x)
+    X = np.empty_like(x)
+    _load().orc_dft(x.size, _ptr(x), _ptr(X), sign)
+    return X
+
+
+def fft(x, sign: int = -1) -> np.ndarray:
+    X = _c128(x).copy()
+    n = X.size
+    if n & (n - 1):
+        raise ValueError("radix-2 oracle FFT needs a power of two")
+    _load().orc_fft(n, _ptr(X), sign)
+    return X
+
+
+# ----------------------------------------------------------------------------- method
+def iono(x, fs: float, fc: float, tec: float, direct: bool = False, distort: bool = False) -> np.ndarray:
+    """Eq. 15 correction (distort=False) or Eq. 14 distortion (distort=True) of one pulse."""
+    x = _c128(x)
+    y = np.empty_like(x)
+    n = x.size
+    if not direct and (n & (n - 1)):
+        raise ValueError("radix-2 path needs a power of two; use direct=True")
+    rc = _load().orc_iono_dir(n, fs, fc, tec, +1 if distort else -1, 1 if direct else 0,
+                              _ptr(x), _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_iono_dir failed ({rc})")
+    return y
+
+
+def doppler(x, W: int, fs: float, fc: float, alpha: float) -> np.ndarray:
+    """Windowed Whittaker-Shannon resampling onto t/alpha, Eq. 16 + window."""
+    x = _c128(x)
+    y = np.empty_like(x)
+    rc = _load().orc_doppler(x.size, int(W), fs, fc, alpha, _ptr(x), _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_doppler failed ({rc})")
+    return y
+
+
+def doppler_exact(x, fs: float, fc: float, alpha: float) -> np.ndarray:
+    """Unwindowed Eq. 16 (O(n^2)) -- brute-force pin only."""
+    x = _c128(x)
+    y = np.empty_like(x)
+    _load().orc_doppler_exact(x.size, fs, fc, alpha, _ptr(x), _ptr(y))
+    return y
+
+
+def correct(x, W: int, fs: float, fc: float, tec: float, alpha: float) -> np.ndarray:
+    """dc_correct = doppler(iono(x)), iono first (reading R7)."""
+    return doppler(iono(x, fs, fc, tec), W, fs, fc, alpha)
+
+
+STAGES = {"iono": 1, "doppler": 2, "correct": 3}
+
+
+def run_batch(stage: str, x64: np.ndarray, fs: float, fc: float, W: int,
+              tec=None, alpha=None, nthreads: int = 0, direct: bool = False) -> np.ndarray:
+    """Batched oracle on complex64 input [batch, n] (upcast exactly), complex128 output."""
+    x64 = np.ascontiguousarray(x64, dtype=np.complex64)
+    if x64.ndim == 1:
+        x64 = x64[None]
+    batch, n = x64.shape
+    tec_a = np.ascontiguousarray(np.zeros(batch) if tec is None else np.broadcast_to(tec, (batch,)), dtype=np.float64)
+    alpha_a = np.ascontiguousarray(np.ones(batch) if alpha is None else np.broadcast_to(alpha, (batch,)), dtype=np.float64)
+    y = np.empty((batch, n), dtype=np.complex128)
+    rc = _load().orc_run_batch(STAGES[stage], n, batch, fs, fc, int(W), _ptr(tec_a), _ptr(alpha_a),
+                               _ptr(x64), _ptr(y), int(nthreads), 1 if direct else 0)
+    if rc:
+        raise RuntimeError(f"orc_run_batch failed ({rc})")
+    return y
+
+
+def max_threads() -> int:
+    return _load().orc_max_threads()

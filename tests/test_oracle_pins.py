@@ -1,0 +1,345 @@
+"""Pins of the FP64 oracle against what the paper and mathematics fix (CPU only).
+
+Each test names the passage it pins.  These tests must catch a dropped term,
+a wrong sign, a wrong index or a transposed operand anywhere in oracle/.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import lfm as L
+from oracle import oracle as O
+from golden_io import read_golden
+
+C = 299792458.0
+
+
+# --------------------------------------------------------------------------- constants (Eq. 1, Eq. 13)
+def test_k2_constant_standard_value(golden_dir):
+    rows = dict((r[0], r[1]) for r in read_golden(os.path.join(golden_dir, "paper_values.txt")))
+    approx, tol = float(rows["k2_per_tec_approx"]), float(rows["k2_per_tec_reltol"])
+    k = O.k2_per_tec()
+    assert abs(k / approx - 1) < tol                       # ~40.31
+    assert abs(k - 40.308193022) < 1e-8                     # CODATA 2018 closed form
+
+
+def test_group_delay_values():
+    # tau(413 MHz, 1e18) ~ 7.88e-7 s
+    assert abs(O.group_delay(413e6, 1e18) - 7.882655e-7) < 1e-12
+    # f^-2 scaling (Eq. 1): tau(2f) = tau(f)/4 and linear in TEC
+    assert O.group_delay(826e6, 1e18) == pytest.approx(O.group_delay(413e6, 1e18) / 4, rel=1e-15)
+    assert O.group_delay(413e6, 2e18) == pytest.approx(2 * O.group_delay(413e6, 1e18), rel=1e-15)
+    assert O.group_delay(413e6, 0.0) == 0.0
+    # phase scale nu(413 MHz, 100 TECU) = 651.107 cycles = 2 tau f (two-way)
+    assert O.iono_phase_cycles(413e6, 1e18) == pytest.approx(651.1073, abs=1e-3)
+    assert O.iono_phase_cycles(-1e6, 1e18) == 0.0 and O.iono_phase_cycles(0.0, 1e18) == 0.0
+
+
+def test_alpha_from_velocity():
+    assert O.alpha_from_velocity(0.0) == 1.0
+    assert O.alpha_from_velocity(5000.0) - 1 == pytest.approx(3.33569658541e-5, rel=1e-9)
+    for v in (1e3, 1e4, 1e5, 1e6):
+        assert abs(O.alpha_from_velocity(v) * O.alpha_from_velocity(-v) - 1) < 1e-15
+    assert O.alpha_from_velocity(1000.0) > 1  # approaching => alpha > 1
+
+
+# --------------------------------------------------------------------------- DFT core
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 12, 16, 64, 100])
+def test_direct_dft_vs_numpy(n):
+    x = synth.complex_gaussian(n, seed=n)
+    assert np.allclose(O.dft(x, -1), np.fft.fft(x), rtol=0, atol=1e-12 * max(1, n))
+    assert np.allclose(O.dft(x, +1) / n, np.fft.ifft(x), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("p", list(range(1, 13)))
+def test_radix2_fft_vs_direct_and_numpy(p):
+    n = 1 << p
+    x = synth.complex_gaussian(n, seed=100 + p)
+    X = O.fft(x)
+    ref = np.fft.fft(x)
+    assert np.linalg.norm(X - ref) / np.linalg.norm(ref) < 1e-13
+    if n <= 1024:
+        D = O.dft(x)
+        assert np.linalg.norm(X - D) / np.linalg.norm(D) < 1e-13
+    assert np.linalg.norm(O.fft(X, +1) / n - x) / np.linalg.norm(x) < 1e-14
+
+
+def test_radix2_fft_large_vs_numpy():
+    n = 1 << 18
+    x = synth.complex_gaussian(n, seed=7)
+    X = O.fft(x)
+    ref = np.fft.fft(x)
+    assert np.linalg.norm(X - ref) / np.linalg.norm(ref) < 1e-12
+
+
+# --------------------------------------------------------------------------- iono: Eq. 15 / Eq. 14
+def test_bin_frequency_mapping():
+    n, fs, fc = 16, 1.6e9, 0.0
+    f = [O.bin_frequency(k, n, fs, fc) for k in range(n)]
+    assert np.allclose(f, fc + np.fft.fftfreq(n, 1 / fs))  # numpy convention; Nyquist bin negative
+    assert O.bin_frequency(8, 16, 16.0, 100.0) == 92.0
+
+
+def test_iono_tec0_identity():
+    x = synth.complex_gaussian(1024, seed=1)
+    y = O.iono(x, 2.048e9, 0.0, 0.0)
+    assert np.max(np.abs(y - x)) < 1e-14
+
+
+def test_iono_golden_impulse(golden_dir):
+    rows = read_golden(os.path.join(golden_dir, "G1_iono_impulse.txt"))
+    p = [r for r in rows if r[0] == "params"][0]
+    n, fs, fc, tec = int(p[1]), float(p[2]), float(p[3]), float(p[4])
+    x = np.zeros(n, complex)
+    x[0] = 1
+    y = O.iono(x, fs, fc, tec)
+    yd = O.iono(x, fs, fc, tec, direct=True)
+    for r in rows:
+        if r[0] == "nu":
+            k = int(r[1])
+            assert O.iono_phase_cycles(O.bin_frequency(k, n, fs, fc), tec) == pytest.approx(float(r[2]), abs=1e-8)
+        if r[0] == "y":
+            i = int(r[1])
+            assert abs(y[i] - complex(float(r[2]), float(r[3]))) < 1e-11
+            assert abs(yd[i] - complex(float(r[2]), float(r[3]))) < 1e-11
+    assert np.linalg.norm(y) == pytest.approx(1.0, abs=1e-14)
+
+
+def test_iono_golden_bin_tone(golden_dir):
+    rows = read_golden(os.path.join(golden_dir, "G1b_iono_bin_tone.txt"))
+    p = [r for r in rows if r[0] == "params"][0]
+    n, fs, fc, tec = int(p[1]), float(p[2]), float(p[3]), float(p[4])
+    k0 = int([r for r in rows if r[0] == "k0"][0][1])
+    x = synth.bin_tone(n, k0)
+    y = O.iono(x, fs, fc, tec)
+    nu = float([r for r in rows if r[0] == "nu"][0][2])
+    ratio = y / x
+    assert np.ptp(ratio.real) < 1e-13 and np.ptp(ratio.imag) < 1e-13
+    assert abs(ratio[0] - np.exp(-2j * np.pi * nu)) < 1e-9
+    y0 = [r for r in rows if r[0] == "y"][0]
+    assert abs(y[0] - complex(float(y0[2]), float(y0[3]))) < 1e-11
+
+
+@pytest.mark.parametrize("k0", [1, 100, 511, 512, 700, 1023])
+def test_iono_tone_is_eigenvector(k0):
+    # A bin-centred tone is a DFT eigenvector, so Eq. 15 multiplies it by exp(-i 2 pi nu_k0) with
+    # nu = 2 tau(f) f (two-way) at f = fc + fftfreq(k0) -- or by 1 if f <= 0.
+    n, fs, fc, tec = 1024, 1.024e9, 0.0, 3e17
+    x = synth.bin_tone(n, k0)
+    y = O.iono(x, fs, fc, tec)
+    f = np.fft.fftfreq(n, 1 / fs)[k0] + fc
+    nu = 2 * O.group_delay(f, tec) * f if f > 0 else 0.0
+    assert np.max(np.abs(y - x * np.exp(-2j * np.pi * (nu - np.rint(nu))))) < 1e-11
+
+
+def test_iono_parseval_roundtrip_linearity():
+    n, fs = 4096, 2.048e9
+    x1 = synth.complex_gaussian(n, 11)
+    x2 = synth.complex_gaussian(n, 12)
+    y1 = O.iono(x1, fs, 0.0, 1e18)
+    assert abs(np.linalg.norm(y1) / np.linalg.norm(x1) - 1) < 1e-14          # unit-modulus filter
+    back = O.iono(y1, fs, 0.0, 1e18, distort=True)                            # Eq. 14 after Eq. 15
+    assert np.linalg.norm(back - x1) / np.linalg.norm(x1) < 1e-14
+    a, b = 0.3 - 1.2j, 2.0 + 0.5j
+    lhs = O.iono(a * x1 + b * x2, fs, 0.0, 1e18)
+    rhs = a * y1 + b * O.iono(x2, fs, 0.0, 1e18)
+    assert np.linalg.norm(lhs - rhs) / np.linalg.norm(rhs) < 1e-14
+
+
+def test_iono_fft_equals_direct_dft():
+    x = synth.complex_gaussian(512, 5)
+    a = O.iono(x, 51.2e6, 422e6, 7e17)
+    b = O.iono(x, 51.2e6, 422e6, 7e17, direct=True)
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-13
+
+
+@pytest.mark.parametrize("f_carrier", [400e6, 440e6])
+def test_sign_gaussian_packet_group_delay(f_carrier):
+    # Eq. 14 (distortion) delays the envelope by the two-way group delay 2 tau(f);
+    # Eq. 15 (correction) advances it by the same amount.  Closed form: shift = 2 K2/(c f^2) fs samples.
+    n, fs, tec, sigma = 1 << 15, 2.048e9, 1e18, 2000.0
+    x = synth.gaussian_packet(n, fs, f_carrier, sigma, center=n / 2)
+    expect = 2 * O.group_delay(f_carrier, tec) * fs
+    assert expect == pytest.approx(3442.0 if f_carrier == 400e6 else 2844.6, abs=0.1)
+    p0 = L.envelope_peak(x)
+    dist = L.envelope_peak(O.iono(x, fs, 0.0, tec, distort=True)) - p0
+    corr = L.envelope_peak(O.iono(x, fs, 0.0, tec)) - p0
+    assert dist == pytest.approx(expect, abs=2.0)
+    assert corr == pytest.approx(-expect, abs=2.0)
+
+
+# --------------------------------------------------------------------------- Fig. 2 CUBIC pin
+def test_cubic_closed_form_matches_newton_and_golden(golden_dir):
+    rows = read_golden(os.path.join(golden_dir, "G3_cubic.txt"))
+    p = [float(v) for v in [r for r in rows if r[0] == "params"][0][1:]]
+    f0, B, T, tec = p
+    k2 = O.k2_per_tec() * tec
+    t = np.linspace(0, T, 1001)
+    fc = L.cubic_frequency(t, f0, B, T, k2)
+    fn = L.cubic_frequency_newton(t, f0, B, T, k2)
+    assert np.max(np.abs(fc - fn)) < 1e-3                    # Eq. 9-12 vs Eq. 2 by Newton (Hz)
+    assert np.all(np.diff(fc) > 0)
+    for r in rows:
+        if r[0] == "f":
+            assert L.cubic_frequency(np.array([float(r[1])]), f0, B, T, k2)[0] == pytest.approx(float(r[2]), abs=2e-3)
+    # k2 = 0 reduces Eq. 2 to the undistorted chirp f0 + B t / T
+    assert np.allclose(L.cubic_frequency(t, f0, B, T, 0.0), f0 + B * t / T, rtol=0, atol=1e-6)
+
+
+def test_fig2_fft_correction_vs_cubic_truth(golden_dir):
+    # PAPER Fig. 2 caption / P:L305: "CUBIC (*) FFT ... lost < 0.01 dB SNR" at
+    # f0 = 413 MHz, B = 18 MHz, fs = 2.048 GHz, E = 100e16, T = 100 us; N = 2^19.
+    vals = dict((r[0], float(r[1])) for r in read_golden(os.path.join(golden_dir, "paper_values.txt")))
+    f0, B, fs, tec, T = (vals["fig2_f0_hz"], vals["fig2_B_hz"], vals["fig2_fs_hz"], vals["fig2_tec"], vals["fig2_T_s"])
+    n = 1 << 19
+    x = synth.lfm(n, fs, f0, B, T, offset=1 << 17)
+    cub = L.cubic_waveform(f0, B, T, O.k2_per_tec() * tec, fs)
+    loss = L.matched_filter_loss_db(O.iono(x, fs, 0.0, tec), cub)
+    assert loss < vals["fig2_fft_vs_cubic_loss_db_max"]
+    assert loss == pytest.approx(0.00645, abs=5e-4)           # SURVEY 8c reproduction
+    # the flipped sign (a plausible silent mistake) loses dB-scale SNR
+    assert L.matched_filter_loss_db(O.iono(x, fs, 0.0, tec, distort=True), cub) > 5.0
+    # uncorrected dispersion loss (context) ~1.31 dB
+    assert 1.2 < L.matched_filter_loss_db(x, cub) < 1.4
+    # same pin at baseband: fc = 422 MHz with fs = 204.8 MHz covering 413-431 MHz (reading R2)
+    fsb, fcb, nb = 204.8e6, 422e6, 1 << 15
+    xb = synth.lfm(nb, fsb, f0, B, T, offset=1000, fc=fcb)
+    tb = np.arange(int(round(T * fsb))) / fsb
+    fb = L.cubic_frequency(tb, f0, B, T, O.k2_per_tec() * tec) - fcb
+    cycb = np.concatenate([[0.0], np.cumsum(0.5 * (fb[:-1] + fb[1:]) / fsb)])
+    cubb = np.exp(2j * np.pi * (cycb - np.floor(cycb)))
+    assert L.matched_filter_loss_db(O.iono(xb, fsb, fcb, tec), cubb) < vals["fig2_fft_vs_cubic_loss_db_max"]
+
+
+# --------------------------------------------------------------------------- doppler: Eq. 16 + window
+def test_doppler_alpha_one_bit_exact():
+    x = synth.complex_gaussian(777, 3)
+    for W in (2, 7, 16, 32):
+        y = O.doppler(x, W, 2.048e9, 0.0, 1.0)
+        assert np.array_equal(y, x)
+    y = O.doppler(x, 16, 51.2e6, 422e6, 1.0)  # carrier term vanishes at beta = 1
+    assert np.array_equal(y, x)
+
+
+def test_doppler_golden(golden_dir):
+    rows = read_golden(os.path.join(golden_dir, "G2_doppler.txt"))
+    cases = {r[1]: (int(r[2]), float(r[3])) for r in rows if r[0] == "case"}
+    x = np.arange(16) + 1j * (16 - np.arange(16))
+    out = {name: O.doppler(x, W, 16e6, fc, 1.25) for name, (W, fc) in cases.items()}
+    for r in rows:
+        if r[0] == "y":
+            assert abs(out[r[1]][int(r[2])] - complex(float(r[3]), float(r[4]))) < 1e-10
+
+
+def test_doppler_integer_positions_direction():
+    # alpha = 2 => beta = 1/2: output m samples the input at t = m/2 (resampling onto t/alpha,
+    # undoing S(alpha t), Eq. 13).  At integer t the normalised sinc is a Kronecker delta.
+    x = synth.complex_gaussian(64, 9)
+    y = O.doppler(x, 8, 1.0, 0.0, 2.0)
+    assert np.array_equal(y[0::2], x[:32])
+    # alpha = 1/2 => beta = 2: y[m] = x[2m] inside the record, 0 past its end (zeros outside, R12)
+    y = O.doppler(x, 8, 1.0, 0.0, 0.5)
+    assert np.array_equal(y[:32], x[0::2]) and np.all(y[32:] == 0)
+
+
+@pytest.mark.parametrize("n", [8, 33, 64])
+def test_doppler_full_window_equals_exact(n):
+    # With W/2 > max(t) + n the window covers the whole record: windowed Eq. 16 == exact Eq. 16.
+    x = synth.complex_gaussian(n, n)
+    for alpha in (1.0 + 3e-5, 0.93, 1.21):
+        a = O.doppler(x, 3 * n + 2, 1e6, 0.0, alpha)
+        b = O.doppler_exact(x, 1e6, 0.0, alpha)
+        assert np.max(np.abs(a - b)) < 1e-12
+
+
+def test_doppler_window_membership_odd_even():
+    # odd W: the W samples nearest to t (centre = nearest sample);
+    # even W: {k : -W/2 < k - t <= W/2}.
+    n = 40
+    x = np.zeros(n, complex)
+    alpha = 1 / 1.3  # beta = 1.3
+    for W in (4, 5):
+        for k in range(n):
+            x[:] = 0
+            x[k] = 1
+            y = O.doppler(x, W, 1.0, 0.0, alpha)
+            for m in range(n):
+                t = m * 1.3
+                inside = (-W / 2 < k - t <= W / 2)
+                if not inside:
+                    assert y[m] == 0
+                elif abs(t - round(t)) > 1e-9:
+                    assert y[m] != 0
+
+
+def test_doppler_recovers_dilated_lfm_and_error_falls_with_W():
+    # Analytic truth (Table 2 "Analytical Resampling"): the echo S(alpha t) of a Tukey LFM, corrected
+    # by resampling onto t/alpha, must approach the undilated chirp; error drops with W (Table 2
+    # "O(N_window^-2)").  Resampling the wrong way (alpha -> 1/alpha) must be much worse.
+    n, fs = 1 << 14, 2.048e9
+    T = 0.8 * n / fs
+    alpha = O.alpha_from_velocity(5000.0)
+    t = np.arange(n) / fs
+    truth = _tukey_at(t - (n // 10) / fs, T)
+    echo = _tukey_at(alpha * t - (n // 10) / fs, T)     # S(alpha t)
+    nrm = np.linalg.norm(truth)
+    errs = [np.linalg.norm(O.doppler(echo, W, fs, 0.0, alpha) - truth) / nrm for W in (8, 16, 32)]
+    unc = np.linalg.norm(echo - truth) / nrm
+    wrong = np.linalg.norm(O.doppler(echo, 32, fs, 0.0, 1 / alpha) - truth) / nrm
+    assert errs[0] > errs[1] > errs[2]
+    assert errs[2] < 0.02 and unc > 10 * errs[2] and wrong > unc
+
+
+def _tukey_at(tau, T, f0=411e6, B=18e6, frac=0.1):
+    inside = (tau >= 0) & (tau < T)
+    cyc = f0 * tau + 0.5 * B * tau * tau / T
+    x = np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+    u = np.clip(tau / T, 0, 1)
+    env = np.ones_like(u)
+    a = frac / 2
+    lo, hi = u < a, u > 1 - a
+    env[lo] = 0.5 * (1 - np.cos(np.pi * u[lo] / a))
+    env[hi] = 0.5 * (1 - np.cos(np.pi * (1 - u[hi]) / a))
+    x = x * env
+    x[~inside] = 0
+    return x
+
+
+def test_doppler_carrier_term_baseband():
+    # Baseband samples with an LO at fc: the echo of S_RF(alpha t) is s_bb(alpha t) exp(i 2 pi fc (alpha-1) t).
+    # Resampling onto t/alpha must be followed by exp(-i 2 pi fc (1 - beta) t) (reading R10); without
+    # it (fc passed as 0) the residual carrier costs a large loss.
+    n, fs, fc, T = 4096, 51.2e6, 422e6, 40e-6
+    alpha = O.alpha_from_velocity(5000.0)
+    t = np.arange(n) / fs
+    off = 48 / fs
+    def sbb(tt):
+        tau = tt - off
+        inside = (tau >= 0) & (tau < T)
+        cyc = (413e6 - fc) * tau + 0.5 * 18e6 * tau * tau / T
+        v = np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+        v[~inside] = 0
+        return v
+    truth = sbb(t)
+    cyc = fc * (alpha - 1) * t
+    echo = sbb(alpha * t) * np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+    with_c = L.matched_filter_loss_db(O.doppler(echo, 32, fs, fc, alpha), truth)
+    without = L.matched_filter_loss_db(O.doppler(echo, 32, fs, 0.0, alpha), truth)
+    assert with_c < 0.01
+    assert without > 0.1
+
+
+def test_batch_entry_matches_single_and_is_thread_independent():
+    n, batch, fs = 1024, 5, 2.048e9
+    x = synth.complex_gaussian(n, 21, batch=batch).astype(np.complex64)
+    tec, alpha = synth.pulse_params(batch)
+    y1 = O.run_batch("correct", x, fs, 0.0, 16, tec, alpha, nthreads=1)
+    y4 = O.run_batch("correct", x, fs, 0.0, 16, tec, alpha, nthreads=4)
+    assert np.array_equal(y1, y4)
+    for p in range(batch):
+        ref = O.correct(x[p].astype(np.complex128), 16, fs, 0.0, tec[p], alpha[p])
+        assert np.array_equal(y1[p], ref)
+    yi = O.run_batch("iono", x, fs, 0.0, 16, tec, alpha)
+    assert np.array_equal(yi[2], O.iono(x[2].astype(np.complex128), fs, 0.0, tec[2]))
