@@ -18,8 +18,9 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# overridable only for the mutation check in tools/mutate_oracle.py
+_SRC = os.environ.get("DISPCORR_ORACLE_SRC", os.path.join(_HERE, "oracle.c"))
+_LIB = os.environ.get("DISPCORR_ORACLE_LIB", os.path.join(_HERE, "liboracle.so"))
 
 _lib = None
 

@@ -1,0 +1,45 @@
+"""Mutation check of the oracle pins: each plausible mistake in oracle/oracle.c must fail a
+`-m "not gpu"` oracle pin test.  Run: python tools/mutate_oracle.py"""
+import os
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = open(os.path.join(ROOT, "oracle", "oracle.c")).read()
+
+MUTANTS = {
+    "flip iono sign": ("return orc_iono_dir(n, fs, fc, tec, -1, method, x, y);", "return orc_iono_dir(n, fs, fc, tec, +1, method, x, y);"),
+    "one-way delay": ("return 2.0 * k2 / (ORC_C * f_hz);", "return k2 / (ORC_C * f_hz);"),
+    "K2 uses 4 pi^2": ("(8.0 * ORC_PI * ORC_PI * ORC_ME * ORC_EPS0)", "(4.0 * ORC_PI * ORC_PI * ORC_ME * ORC_EPS0)"),
+    "Nyquist bin positive": ("(k >= n / 2) ? k - n : k", "(k > n / 2) ? k - n : k"),
+    "no fc offset": ("return fc + fs * (double)kk / (double)n;", "return fs * (double)kk / (double)n;"),
+    "no 1/n": ("for (int64_t t = 0; t < 2 * n; ++t) y[t] /= (double)n;", ""),
+    "fft twiddle sign": ("double ang = (double)sign * 2.0 * ORC_PI * (double)j / (double)len;", "double ang = -(double)sign * 2.0 * ORC_PI * (double)j / (double)len;"),
+    "window off by one": ("int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W) + 1;", "int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W);"),
+    "resample at alpha": ("double beta = 1.0 / alpha;\n  for (int64_t m = 0; m < n; ++m) {\n    double t = (double)m * beta;\n    int64_t k_lo", "double beta = alpha;\n  for (int64_t m = 0; m < n; ++m) {\n    double t = (double)m * beta;\n    int64_t k_lo"),
+    "carrier sign": ("    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* Exact", "    double ang = 2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* Exact"),
+    "sinc missing pi": ("return sin(ORC_PI * d) / (ORC_PI * d);", "return sin(ORC_PI * d) / (d);"),
+    "conj multiply": ("X[2 * k + 1] = xr * s + xi * c;", "X[2 * k + 1] = -xr * s + xi * c;"),
+    "drop last sample": ("if (k < 0 || k >= n) continue;", "if (k < 0 || k >= n - 1) continue;"),
+    "no u==0 sinc case": ("if (d == 0.0) return 1.0;\n  if (d == floor(d)) return 0.0;", "if (d == 0.0) return 1.0;"),
+}
+
+failed_to_catch = []
+with tempfile.TemporaryDirectory() as d:
+    for name, (a, b) in [(k, v) for k, v in MUTANTS.items() if len(sys.argv) < 2 or k in sys.argv[1:]]:
+        assert a in SRC, name
+        src = os.path.join(d, "m.c")
+        lib = os.path.join(d, "m.so")
+        open(src, "w").write(SRC.replace(a, b, 1))
+        if os.path.exists(lib):
+            os.remove(lib)
+        env = dict(os.environ, DISPCORR_ORACLE_SRC=src, DISPCORR_ORACLE_LIB=lib)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_oracle_pins.py"], cwd=ROOT, env=env,
+                           capture_output=True, text=True, timeout=300)
+        caught = r.returncode != 0
+        print(f"{'CAUGHT ' if caught else 'MISSED '} {name}")
+        if not caught:
+            failed_to_catch.append(name)
+print("all mutants caught" if not failed_to_catch else f"missed: {failed_to_catch}")
+sys.exit(1 if failed_to_catch else 0)
