@@ -1,0 +1,141 @@
+/*
+ * libdispcorr -- B200-native (sm_100a) per-pulse dispersion correction.
+ *
+ * C ABI of the hot path of arXiv 2508.04951 (Vickers, Mack, Osaretin):
+ *   stage 1, ionospheric correction (Eq. 15):
+ *       S_Tx = F^-1[ F(S_Rx) exp(-4 pi i K2 / (c f)) ],   K2 = 40.308193022 * TEC   (Eq. 1)
+ *   stage 2, Doppler time-dilation correction (Eq. 13; Eq. 16):
+ *       windowed Whittaker-Shannon (sinc) resampling of each pulse onto t/alpha
+ *       using the W samples around each output.
+ * Readings of silent passages (bin -> frequency map, window membership, carrier
+ * term, ...) are DESIGN.md R1..R13; they are restated at each call below.
+ *
+ * Conventions shared by every call
+ *   - Samples are complex64: interleaved (re, im) IEEE float32 pairs,
+ *     laid out pulse-major, float2[batch][n]; pulse p starts at x + p*n.
+ *   - Device pointers must be CUDA device (or managed) memory of the plan's
+ *     device, 16-byte aligned (torch allocations are 256-byte aligned).
+ *   - Per-pulse parameter arrays (tec, alpha) are HOST arrays of `batch`
+ *     binary64 values; they are validated and copied before the call returns,
+ *     so the caller may reuse them immediately.
+ *   - Calls are asynchronous on the plan's stream: DC_OK means "validated and
+ *     enqueued".  Asynchronous faults surface as DC_ERR_CUDA from the next call
+ *     or from dc_sync().  dc_correct_host() is the one synchronous call.
+ *   - A plan must not be used from two host threads at once (it owns scratch and
+ *     a parameter staging ring).  Distinct plans are independent.
+ *   - Errors are synchronous and nothing is enqueued when a call returns an
+ *     error; dc_last_error_message() gives a one-line explanation.
+ */
+#ifndef LIBDISPCORR_H
+#define LIBDISPCORR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DC_VERSION 100 /* 1.0.0 */
+
+typedef struct dc_plan_s *dc_plan_t; /* opaque; created by dc_plan, destroyed by dc_plan_destroy */
+
+typedef enum {
+  DC_OK = 0,
+  DC_ERR_INVALID_VALUE = 1,      /* a size / rate / parameter outside its documented range */
+  DC_ERR_NULL_POINTER = 2,       /* a required pointer is NULL */
+  DC_ERR_MISALIGNED = 3,         /* a sample pointer is not 16-byte aligned */
+  DC_ERR_ALIASING = 4,           /* y overlaps x where the call requires distinct buffers */
+  DC_ERR_OUT_OF_MEMORY = 5,      /* device or pinned-host allocation failed */
+  DC_ERR_CUDA = 6,               /* a CUDA runtime error (incl. an earlier asynchronous fault) */
+  DC_ERR_UNSUPPORTED_DEVICE = 7, /* device is not compute capability 10.0 (B200, sm_100a) */
+  DC_ERR_NOT_DEVICE_MEMORY = 8   /* a sample pointer is not device/managed memory of the plan's device */
+} dc_status;
+
+/* Plan for pulses of n complex samples at sample rate fs_hz whose DFT bin k
+ * represents absolute frequency f_k = fc_hz + fs_hz*(k - n*[k >= n/2])/n
+ * (reading R2; fc_hz = 0 for absolute-RF complex samples as in P:L311), with a
+ * W = taps sample sinc window for the Doppler stage.
+ *   n      power of two, 2 <= n <= 2^24 (O(N log N) for N = 2^k)
+ *   fs_hz  > 0, finite;  fc_hz >= 0, finite
+ *   taps   2 <= taps <= 128 and taps <= n (odd or even)
+ *   device CUDA device ordinal (must be sm_100)
+ *   cuda_stream  cudaStream_t to enqueue on; NULL = legacy default stream
+ * Allocates the plan's device scratch, twiddle tables and pinned staging; no
+ * kernel runs.  On error *out is set to NULL. */
+dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int taps, int device,
+                  void *cuda_stream);
+
+/* Release everything the plan owns (synchronises the plan's stream first). */
+dc_status dc_plan_destroy(dc_plan_t plan);
+
+/* Re-target the plan to another stream of the same device. */
+dc_status dc_set_stream(dc_plan_t plan, void *cuda_stream);
+
+/* Block until all work enqueued by this plan is done; reports asynchronous faults. */
+dc_status dc_sync(dc_plan_t plan);
+
+/* Ionospheric correction, Eq. 15, IN PLACE on device x[batch][n]:
+ *   X = DFT(x) (forward kernel e^{-i 2 pi k t / n});  X_k *= exp(-i 2 pi nu_k) / n with
+ *   nu_k = 2 K2 / (c f_k), K2 = dc_k2_per_tec() * tec[p]  (two-way), nu_k = 0 if f_k <= 0
+ *   (reading R3); x = IDFT(X).  tec: host double[batch], el/m^2, each finite and >= 0.
+ * batch >= 1.  One HBM round trip per pulse for n <= 8192; n > 8192 uses a three-pass
+ * four-step decomposition in place on x. */
+dc_status dc_iono(dc_plan_t plan, void *x, int64_t batch, const double *tec);
+
+/* Forward ionospheric model, Eq. 14: the same with exp(+i 2 pi nu_k).
+ * Used to synthesise dispersed echoes and the matched-filter reference. */
+dc_status dc_iono_distort(dc_plan_t plan, void *x, int64_t batch, const double *tec);
+
+/* Doppler correction: y[p][m] = e^{-i 2 pi fc (1 - beta) m / fs} *
+ *   sum_{k : -W/2 < k - t_m <= W/2, 0 <= k < n} x[p][k] sinc(t_m - k),   t_m = m * beta,
+ *   beta = 1/alpha[p] (binary64), sinc(d) = sin(pi d)/(pi d), sinc(0) = 1   (Eq. 16 windowed;
+ *   readings R8-R12).  Output length n; samples outside [0, n) are zero.
+ * x, y: device float2[batch][n], must not overlap.  alpha: host double[batch], each finite > 0.
+ * alpha[p] == 1 reproduces x[p] bit-exactly. */
+dc_status dc_doppler(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *alpha);
+
+/* dc_correct = dc_doppler(dc_iono(x)) (iono first, reading R7), x left unchanged,
+ * result in y (must not overlap x).  The iono result is kept in a plan-owned,
+ * L2-sized chunk buffer between the stages. */
+dc_status dc_correct(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *tec,
+                     const double *alpha);
+
+/* dc_correct on HOST buffers (pageable or pinned), synchronous: chunks of pulses are
+ * copied host->device, corrected and copied back with copy/compute overlap on the
+ * plan's stream plus an internal copy stream.  x_host, y_host: complex64[batch][n]. */
+dc_status dc_correct_host(dc_plan_t plan, const void *x_host, void *y_host, int64_t batch,
+                          const double *tec, const double *alpha);
+
+/* Plan introspection (for tests and the benchmark). */
+typedef struct {
+  int64_t n;             /* samples per pulse */
+  int log2n;
+  int taps;              /* sinc window W */
+  int regime;            /* 0 = single-CTA fused FFT (n <= 8192), 1 = three-pass four-step */
+  int64_t n1, n2;        /* four-step split n = n1 * n2 (t = n2 t1 + t2, k = k1 + n1 k2); 0 if regime 0 */
+  int64_t chunk_pulses;  /* pulses per dc_correct chunk (scratch = chunk_pulses * n * 8 bytes) */
+  int64_t scratch_bytes; /* device scratch owned by the plan */
+  int sm_count;          /* multiprocessors of the plan's device */
+  int64_t kernel_launches; /* kernels this plan has launched so far */
+} dc_plan_info_t;
+dc_status dc_plan_info(dc_plan_t plan, dc_plan_info_t *info);
+
+/* Human-readable name of a status code (static string). */
+const char *dc_status_string(dc_status s);
+
+/* One-line explanation of the most recent error on the calling thread ("" if none). */
+const char *dc_last_error_message(void);
+
+/* alpha = (1 + v/c) / (1 - v/c), v > 0 approaching; NaN if |v| >= c or v not finite. */
+double dc_alpha_from_velocity(double v_r_mps);
+
+/* K2 / TEC = q_e^2 / (8 pi^2 m_e eps0) (Eq. 1, CODATA 2018) = 40.308193022 m^3 s^-2 per el/m^2. */
+double dc_k2_per_tec(void);
+
+int dc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIBDISPCORR_H */

@@ -1,0 +1,229 @@
+"""paper_2508_04951_b200 -- B200-native per-pulse dispersion correction (arXiv 2508.04951).
+
+Thin ctypes binding over the C ABI of ``libdispcorr`` (include/libdispcorr.h).  This
+module only marshals arguments: every step of the hot path (FFT, ionospheric phase,
+inverse FFT, windowed-sinc resampling) runs in the CUDA kernels of the library.  There
+is no CPU fallback: if the shared library is missing or a call fails, an exception is
+raised.
+
+    import torch, paper_2508_04951_b200 as dc
+    plan = dc.Plan(n=1 << 20, fs=2.048e9, fc=0.0, taps=32)
+    plan.iono(x, tec)                 # x: torch.complex64 [batch, n] on cuda, in place (Eq. 15)
+    plan.doppler(x, y, alpha)         # y = resampled onto t/alpha (Eq. 16, windowed)
+    plan.correct(x, y, tec, alpha)    # both stages, iono first
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["Plan", "DispCorrError", "alpha_from_velocity", "k2_per_tec", "library_path", "load", "STATUS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libdispcorr.so")
+_lib = None
+
+STATUS = {
+    0: "DC_OK", 1: "DC_ERR_INVALID_VALUE", 2: "DC_ERR_NULL_POINTER", 3: "DC_ERR_MISALIGNED",
+    4: "DC_ERR_ALIASING", 5: "DC_ERR_OUT_OF_MEMORY", 6: "DC_ERR_CUDA", 7: "DC_ERR_UNSUPPORTED_DEVICE",
+    8: "DC_ERR_NOT_DEVICE_MEMORY",
+}
+
+
+class DispCorrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("log2n", ctypes.c_int), ("taps", ctypes.c_int), ("regime", ctypes.c_int),
+                ("n1", ctypes.c_int64), ("n2", ctypes.c_int64), ("chunk_pulses", ctypes.c_int64),
+                ("scratch_bytes", ctypes.c_int64), ("sm_count", ctypes.c_int), ("kernel_launches", ctypes.c_int64)]
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libdispcorr.so (built by ``python -m paper_2508_04951_b200.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"libdispcorr.so not built ({_LIB_PATH}); run `python -m paper_2508_04951_b200.build`")
+    lib = ctypes.CDLL(_LIB_PATH)
+    i64, i32, d, p = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+    pd = ctypes.POINTER(ctypes.c_double)
+    sigs = {
+        "dc_plan": ([ctypes.POINTER(p), i64, d, d, i32, i32, p], i32),
+        "dc_plan_destroy": ([p], i32),
+        "dc_set_stream": ([p, p], i32),
+        "dc_sync": ([p], i32),
+        "dc_iono": ([p, p, i64, pd], i32),
+        "dc_iono_distort": ([p, p, i64, pd], i32),
+        "dc_doppler": ([p, p, p, i64, pd], i32),
+        "dc_correct": ([p, p, p, i64, pd, pd], i32),
+        "dc_correct_host": ([p, p, p, i64, pd, pd], i32),
+        "dc_plan_info": ([p, ctypes.POINTER(PlanInfo)], i32),
+        "dc_status_string": ([i32], ctypes.c_char_p),
+        "dc_last_error_message": ([], ctypes.c_char_p),
+        "dc_alpha_from_velocity": ([d], d),
+        "dc_k2_per_tec": ([], d),
+        "dc_version": ([], i32),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise DispCorrError(status, load().dc_last_error_message().decode())
+
+
+def alpha_from_velocity(v_mps: float) -> float:
+    """alpha = (1 + v/c)/(1 - v/c), v > 0 approaching."""
+    return load().dc_alpha_from_velocity(float(v_mps))
+
+
+def k2_per_tec() -> float:
+    """K2 / TEC = q_e^2 / (8 pi^2 m_e eps0) (Eq. 1)."""
+    return load().dc_k2_per_tec()
+
+
+def _f64(a, batch: int, name: str):
+    arr = np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (batch,)))
+    return arr, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _dev_ptr(t, name: str, n: int):
+    """(pointer, batch) of a complex64 CUDA tensor shaped [batch, n] or [n]."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor on a CUDA device")
+    if t.dtype != torch.complex64:
+        raise TypeError(f"{name} must be complex64 (got {t.dtype})")
+    if not t.is_cuda:
+        raise TypeError(f"{name} must be on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() % n:
+        raise ValueError(f"{name} has {t.numel()} samples, not a multiple of n = {n}")
+    return ctypes.c_void_p(t.data_ptr()), t.numel() // n
+
+
+def _host_ptr(a, name: str, n: int):
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.complex64 or not a.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous complex64 CPU tensor")
+        return ctypes.c_void_p(a.data_ptr()), a.numel() // n
+    if not (isinstance(a, np.ndarray) and a.dtype == np.complex64 and a.flags.c_contiguous):
+        raise TypeError(f"{name} must be a contiguous complex64 numpy array or CPU tensor")
+    return ctypes.c_void_p(a.ctypes.data), a.size // n
+
+
+class Plan:
+    """A libdispcorr plan for pulses of n samples (power of two, 2..2^24) at fs Hz whose DFT
+    bin k maps to fc + fftfreq(k) Hz, with a `taps`-sample sinc window."""
+
+    def __init__(self, n: int, fs: float, fc: float = 0.0, taps: int = 32, device: int | None = None,
+                 stream=None):
+        import torch
+        lib = load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.n, self.fs, self.fc, self.taps = int(n), float(fs), float(fc), int(taps)
+        h = ctypes.c_void_p()
+        _check(lib.dc_plan(ctypes.byref(h), self.n, self.fs, self.fc, self.taps, self.device,
+                           ctypes.c_void_p(stream.cuda_stream)))
+        self._h = h
+        self._stream = stream
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load().dc_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_stream(self, stream):
+        _check(load().dc_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)))
+        self._stream = stream
+
+    def sync(self):
+        _check(load().dc_sync(self._h))
+
+    def info(self) -> dict:
+        inf = PlanInfo()
+        _check(load().dc_plan_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in PlanInfo._fields_}
+
+    # -- hot path
+    def iono(self, x, tec):
+        """Eq. 15 ionospheric correction of x [batch, n] in place; tec in el/m^2 per pulse."""
+        px, batch = _dev_ptr(x, "x", self.n)
+        tec_a, pt = _f64(tec, batch, "tec")
+        _check(load().dc_iono(self._h, px, batch, pt))
+        return x
+
+    def iono_distort(self, x, tec):
+        """Eq. 14 forward ionospheric model of x [batch, n] in place."""
+        px, batch = _dev_ptr(x, "x", self.n)
+        tec_a, pt = _f64(tec, batch, "tec")
+        _check(load().dc_iono_distort(self._h, px, batch, pt))
+        return x
+
+    def doppler(self, x, y, alpha):
+        """Windowed-sinc resampling of x onto t/alpha into y (distinct buffers)."""
+        px, batch = _dev_ptr(x, "x", self.n)
+        py, by = _dev_ptr(y, "y", self.n)
+        if by != batch:
+            raise ValueError("x and y batch sizes differ")
+        alpha_a, pa = _f64(alpha, batch, "alpha")
+        _check(load().dc_doppler(self._h, px, py, batch, pa))
+        return y
+
+    def correct(self, x, y, tec, alpha):
+        """y = doppler(iono(x)); x is left unchanged."""
+        px, batch = _dev_ptr(x, "x", self.n)
+        py, by = _dev_ptr(y, "y", self.n)
+        if by != batch:
+            raise ValueError("x and y batch sizes differ")
+        tec_a, pt = _f64(tec, batch, "tec")
+        alpha_a, pa = _f64(alpha, batch, "alpha")
+        _check(load().dc_correct(self._h, px, py, batch, pt, pa))
+        return y
+
+    def correct_host(self, x_host, y_host, tec, alpha):
+        """dc_correct on host buffers (numpy complex64 or CPU tensors, pinned for overlap); synchronous."""
+        px, batch = _host_ptr(x_host, "x_host", self.n)
+        py, by = _host_ptr(y_host, "y_host", self.n)
+        if by != batch:
+            raise ValueError("x and y batch sizes differ")
+        tec_a, pt = _f64(tec, batch, "tec")
+        alpha_a, pa = _f64(alpha, batch, "alpha")
+        _check(load().dc_correct_host(self._h, px, py, batch, pt, pa))
+        return y_host

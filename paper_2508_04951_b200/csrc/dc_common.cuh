@@ -1,0 +1,66 @@
+// dc_common.cuh -- shared device helpers of libdispcorr (product path only).
+//
+// Nothing here is shared with oracle/ (the FP64 CPU oracle): the two
+// implementations are independent by construction.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dc {
+
+// ----------------------------------------------------------------------------- physics
+// CODATA 2018 (SI).  Eq. 1 names the symbols only; reading R5.
+constexpr double kQe = 1.602176634e-19;
+constexpr double kMe = 9.1093837015e-31;
+constexpr double kEps0 = 8.8541878128e-12;
+constexpr double kC = 299792458.0;
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+// K2 / TEC = q_e^2 / (8 pi^2 m_e eps0)   (Eq. 1)
+__host__ __device__ inline double k2_per_tec() { return (kQe * kQe) / (8.0 * kPi * kPi * kMe * kEps0); }
+
+// ----------------------------------------------------------------------------- per-pulse parameters
+// Staged from the host once per call (16 B / pulse).
+struct PulseParams {
+  double nu_coef;  // 2 K2 / c = 2 * k2_per_tec * tec / c  [cycles * Hz]; nu_k = nu_coef / f_k  (Eq. 14/15)
+  double beta;     // 1 / alpha (binary64, computed on the host exactly as the oracle does)
+};
+
+// ----------------------------------------------------------------------------- complex float
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ float2 mul_mi(float2 a) {
+  return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+
+// exp(-i 2 pi r) for |r| <= 1/2 via the SFU sin/cos (abs. error ~4e-7).
+__device__ __forceinline__ float2 expm2pi(float r) {
+  float s, c;
+  __sincosf(6.283185307179586f * r, &s, &c);
+  return make_float2(c, -s);
+}
+
+// Reciprocal of a positive-or-negative binary64 value to ~1 ulp: FP32 SFU seed + 2 Newton steps.
+__device__ __forceinline__ double drcp(double f) {
+  float ff = __double2float_rn(f);
+  float r0;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(ff));
+  double r = (double)r0;
+  double e = fma(-f, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-f, r, 1.0);
+  r = fma(r, e, r);
+  return r;
+}
+
+}  // namespace dc

@@ -1,0 +1,71 @@
+// dc_kernels.h -- internal launch interface between the C-ABI layer and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dc_common.cuh"
+
+namespace dc {
+
+constexpr int kMaxPasses = 8;
+
+// radix sequence of one FFT size, as compiled into the kernels (for twiddle-table building)
+struct PlanDesc {
+  int npass = 0;
+  int log_radix_fwd[kMaxPasses] = {};
+  int log_radix_inv[kMaxPasses] = {};
+  int log_ns_fwd[kMaxPasses] = {};
+  int log_ns_inv[kMaxPasses] = {};
+  int tw_off_fwd[kMaxPasses] = {};
+  int tw_off_inv[kMaxPasses] = {};
+  int tw_size = 0;
+};
+
+bool describe_small_plan(int P, PlanDesc &d);
+bool describe_fourstep_plan(int P, PlanDesc &d);
+void fourstep_split(int log2n, int &P1, int &P2);
+
+struct IonoSmallArgs {
+  const float2 *xin;
+  float2 *xout;
+  int64_t batch;
+  int log2n;
+  const PulseParams *pp;
+  const float2 *twf, *twi;
+  double fs_over_n, fc;
+  cudaStream_t stream;
+};
+cudaError_t launch_iono_small(const IonoSmallArgs &a, bool distort);
+
+struct FourStepArgs {
+  const float2 *src;  // pass A input (pulse-major, pulse_stride apart)
+  float2 *dst;        // passes A/B/C output (may equal src)
+  int64_t pulses;     // pulses in this launch group
+  int64_t pulse_stride;
+  int64_t pulse_base; // index of the first pulse in pp[]
+  int log2n;
+  const PulseParams *pp;
+  const float2 *tw1f, *tw1i;  // N1-point pass tables
+  const float2 *tw2f, *tw2i;  // N2-point pass tables
+  const float2 *twh, *twl;    // outer twiddle two-level table
+  int H;
+  double fs_over_n, fc;
+  cudaStream_t stream;
+};
+cudaError_t launch_iono_fourstep(const FourStepArgs &a, bool distort, int *launches);
+
+struct DopplerArgs {
+  const float2 *x;
+  float2 *y;
+  int64_t pulses;
+  int64_t n;
+  int taps;
+  const PulseParams *pp;
+  int64_t pulse_base;
+  double carrier_cycles_per_sample;  // fc / fs; carrier phase psi_m = fc (1 - beta) m / fs
+  cudaStream_t stream;
+};
+cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1, int *launches);
+int doppler_path(double max_abs_beta_m1);
+
+}  // namespace dc

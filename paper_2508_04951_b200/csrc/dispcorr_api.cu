@@ -1,0 +1,544 @@
+// dispcorr_api.cu -- the libdispcorr C ABI (include/libdispcorr.h): validation, plans,
+// parameter staging, chunk scheduling and kernel dispatch.  No computation of the method
+// happens on the host except per-pulse scalars (2 K2 tec / c and beta = 1/alpha).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/libdispcorr.h"
+#include "dc_kernels.h"
+
+using dc::PulseParams;
+
+namespace {
+
+thread_local char g_errmsg[512] = "";
+
+dc_status fail(dc_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+dc_status fail(dc_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_errmsg, sizeof(g_errmsg), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+dc_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(DC_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define DC_CUDA(call, what)                        \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+constexpr int kRingSlots = 4;
+constexpr int64_t kChunkTargetBytes = 48ll << 20;  // L2-resident working set per chunk (126 MB L2)
+
+struct ParamSlot {
+  PulseParams *host = nullptr;  // pinned
+  PulseParams *dev = nullptr;
+  int64_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool used = false;
+};
+
+}  // namespace
+
+struct dc_plan_s {
+  int64_t n = 0;
+  int log2n = 0;
+  double fs = 0, fc = 0;
+  int taps = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int regime = 0;
+  int P1 = 0, P2 = 0, H = 0;
+  int sm_count = 0;
+  int64_t chunk = 1;  // pulses per chunk
+  // device tables
+  float2 *tw_small_f = nullptr, *tw_small_i = nullptr;
+  float2 *tw1f = nullptr, *tw1i = nullptr, *tw2f = nullptr, *tw2i = nullptr, *twh = nullptr, *twl = nullptr;
+  float2 *scratch = nullptr;  // chunk * n samples
+  int64_t scratch_bytes = 0;
+  // host-path buffers (lazily allocated)
+  float2 *hin[2] = {nullptr, nullptr}, *hout[2] = {nullptr, nullptr};
+  int64_t host_chunk = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  ParamSlot ring[kRingSlots];
+  int ring_next = 0;
+  int64_t launches = 0;
+};
+
+namespace {
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// FP32 twiddle tables generated in binary64: section [NS][R], entry r = exp(-2 pi i k r / (NS R)).
+std::vector<float2> build_pass_tables(const dc::PlanDesc &d, bool inv) {
+  std::vector<float2> t((size_t)std::max(d.tw_size, 2));
+  for (int i = 0; i < d.npass; ++i) {
+    const int lns = inv ? d.log_ns_inv[i] : d.log_ns_fwd[i];
+    const int lr = inv ? d.log_radix_inv[i] : d.log_radix_fwd[i];
+    const int off = inv ? d.tw_off_inv[i] : d.tw_off_fwd[i];
+    const int64_t NS = 1ll << lns, R = 1ll << lr, M = NS * R;
+    for (int64_t k = 0; k < NS; ++k)
+      for (int64_t r = 0; r < R; ++r) {
+        const int64_t e = (k * r) % M;
+        const double ang = -2.0 * dc::kPi * (double)e / (double)M;
+        t[(size_t)(off + k * R + r)] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+  }
+  return t;
+}
+
+dc_status upload(float2 **dst, const std::vector<float2> &src) {
+  DC_CUDA(cudaMalloc(dst, src.size() * sizeof(float2)), "cudaMalloc(twiddles)");
+  DC_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(float2), cudaMemcpyHostToDevice), "cudaMemcpy(twiddles)");
+  return DC_OK;
+}
+
+dc_status check_device_ptr(const dc_plan_s *p, const void *ptr, const char *name) {
+  if (!ptr) return fail(DC_ERR_NULL_POINTER, "%s is NULL", name);
+  if (((uintptr_t)ptr) & 15u) return fail(DC_ERR_MISALIGNED, "%s is not 16-byte aligned", name);
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DC_ERR_NOT_DEVICE_MEMORY, "%s: cudaPointerGetAttributes failed (%s)", name, cudaGetErrorName(e));
+  }
+  if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged))
+    return fail(DC_ERR_NOT_DEVICE_MEMORY, "%s is not device memory", name);
+  if (at.type == cudaMemoryTypeDevice && at.device != p->device)
+    return fail(DC_ERR_NOT_DEVICE_MEMORY, "%s lives on device %d, plan is on device %d", name, at.device, p->device);
+  return DC_OK;
+}
+
+dc_status check_overlap(const void *a, const void *b, int64_t bytes) {
+  const char *pa = (const char *)a, *pb = (const char *)b;
+  if (pa < pb + bytes && pb < pa + bytes) return fail(DC_ERR_ALIASING, "y overlaps x");
+  return DC_OK;
+}
+
+dc_status check_batch(int64_t batch) {
+  if (batch < 1) return fail(DC_ERR_INVALID_VALUE, "batch must be >= 1 (got %lld)", (long long)batch);
+  return DC_OK;
+}
+
+dc_status check_tec(const double *tec, int64_t batch) {
+  if (!tec) return fail(DC_ERR_NULL_POINTER, "tec is NULL");
+  for (int64_t i = 0; i < batch; ++i)
+    if (!std::isfinite(tec[i]) || tec[i] < 0.0)
+      return fail(DC_ERR_INVALID_VALUE, "tec[%lld] = %g must be finite and >= 0", (long long)i, tec[i]);
+  return DC_OK;
+}
+
+dc_status check_alpha(const double *alpha, int64_t batch) {
+  if (!alpha) return fail(DC_ERR_NULL_POINTER, "alpha is NULL");
+  for (int64_t i = 0; i < batch; ++i)
+    if (!std::isfinite(alpha[i]) || !(alpha[i] > 0.0))
+      return fail(DC_ERR_INVALID_VALUE, "alpha[%lld] = %g must be finite and > 0", (long long)i, alpha[i]);
+  return DC_OK;
+}
+
+// Stage per-pulse scalars into a ring slot; returns the device pointer.
+dc_status stage_params(dc_plan_s *p, int64_t batch, const double *tec, const double *alpha, PulseParams **dev,
+                       ParamSlot **slot_out, double *max_abs_beta_m1) {
+  ParamSlot &s = p->ring[p->ring_next];
+  p->ring_next = (p->ring_next + 1) % kRingSlots;
+  if (s.used) DC_CUDA(cudaEventSynchronize(s.done), "cudaEventSynchronize(param slot)");
+  if (s.cap < batch) {
+    if (s.host) cudaFreeHost(s.host);
+    if (s.dev) cudaFree(s.dev);
+    s.host = nullptr;
+    s.dev = nullptr;
+    s.cap = 0;
+    const int64_t cap = std::max<int64_t>(batch, 1024);
+    if (cudaMallocHost(&s.host, sizeof(PulseParams) * cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DC_ERR_OUT_OF_MEMORY, "pinned parameter staging (%lld pulses)", (long long)cap);
+    }
+    if (cudaMalloc(&s.dev, sizeof(PulseParams) * cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DC_ERR_OUT_OF_MEMORY, "device parameter buffer (%lld pulses)", (long long)cap);
+    }
+    s.cap = cap;
+  }
+  const double k2c = 2.0 * dc::k2_per_tec() / dc::kC;  // nu_k = (2 K2 / c) / f_k, two-way
+  double mb = 0.0;
+  for (int64_t i = 0; i < batch; ++i) {
+    s.host[i].nu_coef = tec ? k2c * tec[i] : 0.0;
+    s.host[i].beta = alpha ? 1.0 / alpha[i] : 1.0;
+    mb = std::max(mb, std::fabs(s.host[i].beta - 1.0));
+  }
+  DC_CUDA(cudaMemcpyAsync(s.dev, s.host, sizeof(PulseParams) * batch, cudaMemcpyHostToDevice, p->stream),
+          "cudaMemcpyAsync(params)");
+  *dev = s.dev;
+  *slot_out = &s;
+  if (max_abs_beta_m1) *max_abs_beta_m1 = mb;
+  return DC_OK;
+}
+
+dc_status release_slot(dc_plan_s *p, ParamSlot *s) {
+  DC_CUDA(cudaEventRecord(s->done, p->stream), "cudaEventRecord(param slot)");
+  s->used = true;
+  return DC_OK;
+}
+
+// ---- stage launchers (no validation) -----------------------------------------------------------
+dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
+                   int64_t pulse_base, bool distort) {
+  if (p->regime == 0) {
+    dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp + pulse_base, p->tw_small_f, p->tw_small_i,
+                        p->fs / (double)p->n, p->fc, p->stream};
+    DC_CUDA(dc::launch_iono_small(a, distort), "iono_small_kernel launch");
+    p->launches += 1;
+    return DC_OK;
+  }
+  dc::FourStepArgs a{};
+  a.src = src;
+  a.dst = dst;
+  a.pulses = pulses;
+  a.pulse_stride = p->n;
+  a.pulse_base = pulse_base;
+  a.log2n = p->log2n;
+  a.pp = pp;
+  a.tw1f = p->tw1f;
+  a.tw1i = p->tw1i;
+  a.tw2f = p->tw2f;
+  a.tw2i = p->tw2i;
+  a.twh = p->twh;
+  a.twl = p->twl;
+  a.H = p->H;
+  a.fs_over_n = p->fs / (double)p->n;
+  a.fc = p->fc;
+  a.stream = p->stream;
+  int l = 0;
+  DC_CUDA(dc::launch_iono_fourstep(a, distort, &l), "four-step kernel launch");
+  p->launches += l;
+  return DC_OK;
+}
+
+dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
+                      int64_t pulse_base, double max_abs_beta_m1) {
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, p->stream};
+  int l = 0;
+  DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1, &l), "doppler kernel launch");
+  p->launches += l;
+  return DC_OK;
+}
+
+dc_status iono_common(dc_plan_t p, void *x, int64_t batch, const double *tec, bool distort) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  dc_status s;
+  if ((s = check_batch(batch)) != DC_OK) return s;
+  if ((s = check_device_ptr(p, x, "x")) != DC_OK) return s;
+  if ((s = check_tec(tec, batch)) != DC_OK) return s;
+  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  PulseParams *pp;
+  ParamSlot *slot;
+  if ((s = stage_params(p, batch, tec, nullptr, &pp, &slot, nullptr)) != DC_OK) return s;
+  float2 *xp = (float2 *)x;
+  const int64_t step = (p->regime == 0) ? std::min<int64_t>(batch, 1ll << 30) : p->chunk;
+  for (int64_t b0 = 0; b0 < batch; b0 += step) {
+    const int64_t nb = std::min(step, batch - b0);
+    if ((s = run_iono(p, xp + b0 * p->n, xp + b0 * p->n, nb, pp, b0, distort)) != DC_OK) return s;
+  }
+  return release_slot(p, slot);
+}
+
+}  // namespace
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+const char *dc_status_string(dc_status s) {
+  switch (s) {
+    case DC_OK: return "DC_OK";
+    case DC_ERR_INVALID_VALUE: return "DC_ERR_INVALID_VALUE";
+    case DC_ERR_NULL_POINTER: return "DC_ERR_NULL_POINTER";
+    case DC_ERR_MISALIGNED: return "DC_ERR_MISALIGNED";
+    case DC_ERR_ALIASING: return "DC_ERR_ALIASING";
+    case DC_ERR_OUT_OF_MEMORY: return "DC_ERR_OUT_OF_MEMORY";
+    case DC_ERR_CUDA: return "DC_ERR_CUDA";
+    case DC_ERR_UNSUPPORTED_DEVICE: return "DC_ERR_UNSUPPORTED_DEVICE";
+    case DC_ERR_NOT_DEVICE_MEMORY: return "DC_ERR_NOT_DEVICE_MEMORY";
+  }
+  return "DC_ERR_UNKNOWN";
+}
+
+const char *dc_last_error_message(void) { return g_errmsg; }
+
+int dc_version(void) { return DC_VERSION; }
+
+double dc_k2_per_tec(void) { return dc::k2_per_tec(); }
+
+double dc_alpha_from_velocity(double v) {
+  if (!std::isfinite(v) || std::fabs(v) >= dc::kC) return std::nan("");
+  return (1.0 + v / dc::kC) / (1.0 - v / dc::kC);
+}
+
+dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int taps, int device, void *cuda_stream) {
+  g_errmsg[0] = 0;
+  if (!out) return fail(DC_ERR_NULL_POINTER, "out is NULL");
+  *out = nullptr;
+  if (!is_pow2(n) || n < 2 || n > (1ll << 24))
+    return fail(DC_ERR_INVALID_VALUE, "n = %lld must be a power of two in [2, 2^24]", (long long)n);
+  if (!std::isfinite(fs_hz) || !(fs_hz > 0.0)) return fail(DC_ERR_INVALID_VALUE, "fs_hz = %g must be finite and > 0", fs_hz);
+  if (!std::isfinite(fc_hz) || fc_hz < 0.0) return fail(DC_ERR_INVALID_VALUE, "fc_hz = %g must be finite and >= 0", fc_hz);
+  if (taps < 2 || taps > 128 || taps > n)
+    return fail(DC_ERR_INVALID_VALUE, "taps = %d must be in [2, 128] and <= n", taps);
+  int ndev = 0;
+  DC_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(DC_ERR_INVALID_VALUE, "device %d out of range (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  DC_CUDA(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(DC_ERR_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; libdispcorr is built for sm_100a (B200)", device,
+                prop.major, prop.minor);
+  DC_CUDA(cudaSetDevice(device), "cudaSetDevice");
+
+  dc_plan_s *p = new (std::nothrow) dc_plan_s();
+  if (!p) return fail(DC_ERR_OUT_OF_MEMORY, "plan allocation");
+  p->n = n;
+  p->log2n = 0;
+  while ((1ll << p->log2n) < n) ++p->log2n;
+  p->fs = fs_hz;
+  p->fc = fc_hz;
+  p->taps = taps;
+  p->device = device;
+  p->stream = (cudaStream_t)cuda_stream;
+  p->sm_count = prop.multiProcessorCount;
+  p->regime = (p->log2n <= 13) ? 0 : 1;
+  dc_status s = DC_OK;
+  auto cleanup = [&](dc_status st) {
+    dc_plan_destroy(p);
+    return st;
+  };
+  if (p->regime == 0) {
+    dc::PlanDesc d;
+    dc::describe_small_plan(p->log2n, d);
+    if ((s = upload(&p->tw_small_f, build_pass_tables(d, false))) != DC_OK) return cleanup(s);
+    if ((s = upload(&p->tw_small_i, build_pass_tables(d, true))) != DC_OK) return cleanup(s);
+  } else {
+    dc::fourstep_split(p->log2n, p->P1, p->P2);
+    dc::PlanDesc d1, d2;
+    dc::describe_fourstep_plan(p->P1, d1);
+    dc::describe_fourstep_plan(p->P2, d2);
+    if ((s = upload(&p->tw1f, build_pass_tables(d1, false))) != DC_OK) return cleanup(s);
+    if ((s = upload(&p->tw1i, build_pass_tables(d1, true))) != DC_OK) return cleanup(s);
+    if ((s = upload(&p->tw2f, build_pass_tables(d2, false))) != DC_OK) return cleanup(s);
+    if ((s = upload(&p->tw2i, build_pass_tables(d2, true))) != DC_OK) return cleanup(s);
+    p->H = (p->log2n + 1) / 2;
+    std::vector<float2> lo((size_t)1 << p->H), hi((size_t)1 << (p->log2n - p->H));
+    for (size_t m = 0; m < lo.size(); ++m) {
+      const double a = -2.0 * dc::kPi * (double)m / (double)n;
+      lo[m] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    for (size_t m = 0; m < hi.size(); ++m) {
+      const double a = -2.0 * dc::kPi * (double)(m << p->H) / (double)n;
+      hi[m] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    if ((s = upload(&p->twl, lo)) != DC_OK) return cleanup(s);
+    if ((s = upload(&p->twh, hi)) != DC_OK) return cleanup(s);
+  }
+  p->chunk = std::max<int64_t>(1, kChunkTargetBytes / (n * (int64_t)sizeof(float2)));
+  p->chunk = std::min<int64_t>(p->chunk, 65535);
+  p->scratch_bytes = p->chunk * n * (int64_t)sizeof(float2);
+  if (cudaMalloc(&p->scratch, (size_t)p->scratch_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return cleanup(fail(DC_ERR_OUT_OF_MEMORY, "scratch (%lld bytes)", (long long)p->scratch_bytes));
+  }
+  for (auto &slot : p->ring)
+    if (cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
+  *out = p;
+  return DC_OK;
+}
+
+dc_status dc_plan_destroy(dc_plan_t p) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  cudaSetDevice(p->device);
+  cudaStreamSynchronize(p->stream);
+  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch,
+                    p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
+  for (float2 *b : bufs)
+    if (b) cudaFree(b);
+  for (auto &s : p->ring) {
+    if (s.done) cudaEventDestroy(s.done);
+    if (s.host) cudaFreeHost(s.host);
+    if (s.dev) cudaFree(s.dev);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
+    if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
+    if (p->ev_out[i]) cudaEventDestroy(p->ev_out[i]);
+  }
+  if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+  if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+  delete p;
+  return DC_OK;
+}
+
+dc_status dc_set_stream(dc_plan_t p, void *stream) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  p->stream = (cudaStream_t)stream;
+  return DC_OK;
+}
+
+dc_status dc_sync(dc_plan_t p) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
+  return DC_OK;
+}
+
+dc_status dc_iono(dc_plan_t p, void *x, int64_t batch, const double *tec) {
+  return iono_common(p, x, batch, tec, false);
+}
+
+dc_status dc_iono_distort(dc_plan_t p, void *x, int64_t batch, const double *tec) {
+  return iono_common(p, x, batch, tec, true);
+}
+
+dc_status dc_doppler(dc_plan_t p, const void *x, void *y, int64_t batch, const double *alpha) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  dc_status s;
+  if ((s = check_batch(batch)) != DC_OK) return s;
+  if ((s = check_device_ptr(p, x, "x")) != DC_OK) return s;
+  if ((s = check_device_ptr(p, y, "y")) != DC_OK) return s;
+  if ((s = check_overlap(x, y, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
+  if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
+  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  PulseParams *pp;
+  ParamSlot *slot;
+  double mb = 0;
+  if ((s = stage_params(p, batch, nullptr, alpha, &pp, &slot, &mb)) != DC_OK) return s;
+  const float2 *xp = (const float2 *)x;
+  float2 *yp = (float2 *)y;
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    if ((s = run_doppler(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb)) != DC_OK) return s;
+  }
+  return release_slot(p, slot);
+}
+
+dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const double *tec, const double *alpha) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  dc_status s;
+  if ((s = check_batch(batch)) != DC_OK) return s;
+  if ((s = check_device_ptr(p, x, "x")) != DC_OK) return s;
+  if ((s = check_device_ptr(p, y, "y")) != DC_OK) return s;
+  if ((s = check_overlap(x, y, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
+  if ((s = check_tec(tec, batch)) != DC_OK) return s;
+  if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
+  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  PulseParams *pp;
+  ParamSlot *slot;
+  double mb = 0;
+  if ((s = stage_params(p, batch, tec, alpha, &pp, &slot, &mb)) != DC_OK) return s;
+  const float2 *xp = (const float2 *)x;
+  float2 *yp = (float2 *)y;
+  for (int64_t b0 = 0; b0 < batch; b0 += p->chunk) {
+    const int64_t nb = std::min(p->chunk, batch - b0);
+    if ((s = run_iono(p, xp + b0 * p->n, p->scratch, nb, pp, b0, false)) != DC_OK) return s;
+    if ((s = run_doppler(p, p->scratch, yp + b0 * p->n, nb, pp, b0, mb)) != DC_OK) return s;
+  }
+  return release_slot(p, slot);
+}
+
+dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t batch, const double *tec,
+                          const double *alpha) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  dc_status s;
+  if ((s = check_batch(batch)) != DC_OK) return s;
+  if (!x_host) return fail(DC_ERR_NULL_POINTER, "x_host is NULL");
+  if (!y_host) return fail(DC_ERR_NULL_POINTER, "y_host is NULL");
+  if ((s = check_overlap(x_host, y_host, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
+  if ((s = check_tec(tec, batch)) != DC_OK) return s;
+  if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
+  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  const int64_t hc = p->chunk;  // pulses per transfer chunk
+  if (!p->s_h2d) {
+    DC_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+    DC_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+      DC_CUDA(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming), "cudaEventCreate");
+      DC_CUDA(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming), "cudaEventCreate");
+      DC_CUDA(cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  if (p->host_chunk < hc) {
+    for (int i = 0; i < 2; ++i) {
+      if (p->hin[i]) cudaFree(p->hin[i]);
+      if (p->hout[i]) cudaFree(p->hout[i]);
+      p->hin[i] = p->hout[i] = nullptr;
+    }
+    for (int i = 0; i < 2; ++i) {
+      if (cudaMalloc(&p->hin[i], (size_t)(hc * p->n * sizeof(float2))) != cudaSuccess ||
+          cudaMalloc(&p->hout[i], (size_t)(hc * p->n * sizeof(float2))) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DC_ERR_OUT_OF_MEMORY, "host-path device buffers");
+      }
+    }
+    p->host_chunk = hc;
+  }
+  PulseParams *pp;
+  ParamSlot *slot;
+  double mb = 0;
+  if ((s = stage_params(p, batch, tec, alpha, &pp, &slot, &mb)) != DC_OK) return s;
+  const char *xh = (const char *)x_host;
+  char *yh = (char *)y_host;
+  const size_t pulse_bytes = (size_t)p->n * sizeof(float2);
+  // 3-stage pipeline: H2D (s_h2d) -> correct (plan stream) -> D2H (s_d2h), double-buffered
+  int64_t it = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += hc, ++it) {
+    const int i = (int)(it & 1);
+    const int64_t nb = std::min(hc, batch - b0);
+    if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_comp[i], 0), "wait");  // hin[i] free
+    DC_CUDA(cudaMemcpyAsync(p->hin[i], xh + b0 * pulse_bytes, nb * pulse_bytes, cudaMemcpyHostToDevice, p->s_h2d),
+            "cudaMemcpyAsync(H2D)");
+    DC_CUDA(cudaEventRecord(p->ev_in[i], p->s_h2d), "record");
+    DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[i], 0), "wait");
+    if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[i], 0), "wait");  // hout[i] drained
+    if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, false)) != DC_OK) return s;
+    if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb)) != DC_OK) return s;
+    DC_CUDA(cudaEventRecord(p->ev_comp[i], p->stream), "record");
+    DC_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[i], 0), "wait");
+    DC_CUDA(cudaMemcpyAsync(yh + b0 * pulse_bytes, p->hout[i], nb * pulse_bytes, cudaMemcpyDeviceToHost, p->s_d2h),
+            "cudaMemcpyAsync(D2H)");
+    DC_CUDA(cudaEventRecord(p->ev_out[i], p->s_d2h), "record");
+  }
+  if ((s = release_slot(p, slot)) != DC_OK) return s;
+  DC_CUDA(cudaStreamSynchronize(p->s_d2h), "cudaStreamSynchronize(D2H)");
+  DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
+  return DC_OK;
+}
+
+dc_status dc_plan_info(dc_plan_t p, dc_plan_info_t *info) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  if (!info) return fail(DC_ERR_NULL_POINTER, "info is NULL");
+  info->n = p->n;
+  info->log2n = p->log2n;
+  info->taps = p->taps;
+  info->regime = p->regime;
+  info->n1 = p->regime ? (1ll << p->P1) : 0;
+  info->n2 = p->regime ? (1ll << p->P2) : 0;
+  info->chunk_pulses = p->chunk;
+  info->scratch_bytes = p->scratch_bytes;
+  info->sm_count = p->sm_count;
+  info->kernel_launches = p->launches;
+  return DC_OK;
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path through the C ABI vs the FP64 oracle on identical complex64 inputs.
+
+Bar (north_star): per-pulse relative L2 error <= 1e-5; alpha = 1 bit-exact;
+TEC = 0 within the FP32 FFT round trip.  Sizes span several tiles and ragged tails; the
+full-size configurations are checked on sampled pulses the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import lfm as L
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def dc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2508_04951_b200 as dcmod
+    from paper_2508_04951_b200 import build
+    build.build()
+    dcmod.load()
+    return dcmod
+
+
+def to_dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex64)).cuda()
+
+
+def from_dev(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def rel_l2(a, b):
+    a = np.atleast_2d(a)
+    b = np.atleast_2d(b)
+    num = np.linalg.norm(a - b, axis=1)
+    den = np.maximum(np.linalg.norm(b, axis=1), 1e-300)
+    return num / den
+
+
+def gpu_iono(dc, x, fs, fc, tec, distort=False):
+    p = dc.Plan(x.shape[-1], fs, fc, taps=8)
+    t = to_dev(x)
+    (p.iono_distort if distort else p.iono)(t, tec)
+    return from_dev(t)
+
+
+# ----------------------------------------------------------------------------- iono (Eq. 15)
+@pytest.mark.parametrize("log2n", list(range(1, 14)))
+def test_iono_small_regime_vs_oracle(dc, log2n):
+    n = 1 << log2n
+    batch = 3 if n >= 1024 else 37   # ragged: fewer pulses than a CTA tile holds, or not a multiple
+    x = synth.complex_gaussian(n, seed=log2n, batch=batch).astype(np.complex64)
+    tec = np.linspace(0, 2e18, batch)
+    for fs, fc in ((2.048e9, 0.0), (51.2e6, 422e6)):
+        y = gpu_iono(dc, x, fs, fc, tec)
+        ref = O.run_batch("iono", x, fs, fc, 8, tec)
+        err = rel_l2(y, ref)
+        assert err.max() < TOL, (n, fs, fc, err.max())
+
+
+@pytest.mark.parametrize("log2n", [14, 15, 16, 17, 18, 19, 20])
+def test_iono_fourstep_regime_vs_oracle(dc, log2n):
+    n = 1 << log2n
+    batch = 2
+    x = synth.complex_gaussian(n, seed=100 + log2n, batch=batch).astype(np.complex64)
+    tec = np.array([1e18, 3.7e17])
+    for fs, fc in ((2.048e9, 0.0), (204.8e6, 422e6)):
+        y = gpu_iono(dc, x, fs, fc, tec)
+        ref = O.run_batch("iono", x, fs, fc, 8, tec)
+        err = rel_l2(y, ref)
+        assert err.max() < TOL, (n, fs, fc, err.max())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("log2n", [21, 22, 24])
+def test_iono_largest_pulses_vs_oracle(dc, log2n):
+    n = 1 << log2n
+    x = synth.complex_gaussian(n, seed=log2n, batch=1).astype(np.complex64)
+    y = gpu_iono(dc, x, 2.048e9, 0.0, [1e18])
+    ref = O.run_batch("iono", x, 2.048e9, 0.0, 8, [1e18])
+    assert rel_l2(y, ref).max() < TOL
+
+
+@pytest.mark.parametrize("log2n", [10, 13, 16, 20])
+def test_iono_tec_zero_and_roundtrip(dc, log2n):
+    n = 1 << log2n
+    x = synth.complex_gaussian(n, seed=7, batch=2).astype(np.complex64)
+    y0 = gpu_iono(dc, x, 2.048e9, 0.0, [0.0, 0.0])
+    assert rel_l2(y0, x).max() < 2e-6                       # FFT round trip only
+    d = gpu_iono(dc, x, 2.048e9, 0.0, [1e18, 5e17], distort=True)
+    refd = np.stack([O.iono(x[i].astype(np.complex128), 2.048e9, 0.0, t, distort=True) for i, t in enumerate([1e18, 5e17])])
+    assert rel_l2(d, refd).max() < TOL                      # Eq. 14 path
+    back = gpu_iono(dc, d.astype(np.complex64), 2.048e9, 0.0, [1e18, 5e17])
+    assert rel_l2(back, x).max() < 5e-6                     # Eq. 15 inverts Eq. 14
+
+
+def test_iono_c2_tec_sweep_sampled(dc):
+    # C2: 256 x 2^16 phase-coded pulses, TEC_p = p TECU; parity on sampled pulses, identity at p = 0
+    cfg = synth.c2_batch()
+    x, tec = cfg["x"], cfg["tec"]
+    y = gpu_iono(dc, x, cfg["fs"], 0.0, tec)
+    idx = [0, 1, 17, 128, 255]
+    ref = O.run_batch("iono", x[idx], cfg["fs"], 0.0, 8, tec[idx])
+    assert rel_l2(y[idx], ref).max() < TOL
+    assert rel_l2(y[0], x[0]).max() < 2e-6
+
+
+def test_iono_fig2_cubic_pin_on_gpu(dc):
+    # PAPER Fig. 2: FFT correction vs CUBIC truth loses < 0.01 dB at 2^19 samples
+    n, fs, tec = 1 << 19, 2.048e9, 1e18
+    x = synth.lfm(n, fs, 413e6, 18e6, 100e-6, offset=1 << 17).astype(np.complex64)
+    y = gpu_iono(dc, x[None], fs, 0.0, [tec])[0]
+    cub = L.cubic_waveform(413e6, 18e6, 100e-6, O.k2_per_tec() * tec, fs)
+    assert L.matched_filter_loss_db(y, cub) < 0.01
+
+
+def test_iono_sign_gaussian_packet_on_gpu(dc):
+    n, fs, tec = 1 << 15, 2.048e9, 1e18
+    x = synth.gaussian_packet(n, fs, 400e6, 2000.0, n / 2).astype(np.complex64)
+    y = gpu_iono(dc, x[None], fs, 0.0, [tec])[0]
+    shift = L.envelope_peak(y) - L.envelope_peak(x)
+    assert shift == pytest.approx(-2 * O.group_delay(400e6, tec) * fs, abs=2.0)
+
+
+# ----------------------------------------------------------------------------- doppler (Eq. 16 windowed)
+def gpu_doppler(dc, x, W, fs, fc, alpha):
+    import torch
+    p = dc.Plan(x.shape[-1], fs, fc, taps=W)
+    t = to_dev(x)
+    y = torch.empty_like(t)
+    p.doppler(t, y, alpha)
+    return from_dev(y)
+
+
+ALPHA_CASES = {
+    "fast1": [1 + 3.3e-5, 1 - 3.3e-5, 1 + 1e-5],      # |v| <= 5 km/s: first-order path
+    "fast2": [1 + 4e-4, 1 - 4.5e-4, 1 + 1e-4],        # second-order path
+    "exact": [1.05, 0.93, 1.0 + 2e-3],                # exact-tap path
+}
+
+
+@pytest.mark.parametrize("case", list(ALPHA_CASES))
+@pytest.mark.parametrize("W", [2, 3, 8, 16, 25, 32, 64, 128])
+def test_doppler_vs_oracle(dc, case, W):
+    n = 4096
+    alphas = np.array(ALPHA_CASES[case])
+    x = synth.complex_gaussian(n, seed=W, batch=len(alphas)).astype(np.complex64)
+    for fs, fc in ((2.048e9, 0.0), (51.2e6, 422e6)):
+        y = gpu_doppler(dc, x, W, fs, fc, alphas)
+        ref = O.run_batch("doppler", x, fs, fc, W, None, alphas)
+        err = rel_l2(y, ref)
+        assert err.max() < TOL, (case, W, fs, fc, err.max())
+
+
+@pytest.mark.parametrize("log2n", [4, 11, 16, 20])
+def test_doppler_sizes_vs_oracle(dc, log2n):
+    n = 1 << log2n
+    alphas = np.array([1 + 3.3e-5, 1 - 2e-5])
+    x = synth.complex_gaussian(n, seed=log2n, batch=2).astype(np.complex64)
+    y = gpu_doppler(dc, x, 32 if n >= 32 else n, 2.048e9, 0.0, alphas)
+    ref = O.run_batch("doppler", x, 2.048e9, 0.0, 32 if n >= 32 else n, None, alphas)
+    assert rel_l2(y, ref).max() < TOL
+
+
+@pytest.mark.parametrize("W", [8, 32, 128])
+def test_doppler_alpha_one_bit_exact(dc, W):
+    x = synth.complex_gaussian(8192, seed=3, batch=3).astype(np.complex64)
+    y = gpu_doppler(dc, x, W, 51.2e6, 422e6, [1.0, 1.0, 1.0])
+    assert np.array_equal(y, x)
+
+
+def test_doppler_full_window_equals_exact_eq16(dc):
+    # W = n = 128 and a signal supported on [56, 72): every output whose window (t - 64, t + 64]
+    # covers the support equals the exact (unwindowed) Eq. 16 sum.
+    n, W = 128, 128
+    x = np.zeros((2, n), np.complex64)
+    x[:, 56:72] = synth.complex_gaussian(16, seed=5, batch=2)
+    alphas = [1 + 3e-5, 1.0 + 1e-3]
+    y = gpu_doppler(dc, x, W, 1e6, 0.0, alphas)
+    for i, a in enumerate(alphas):
+        ref = O.doppler_exact(x[i].astype(np.complex128), 1e6, 0.0, a)
+        t = np.arange(n) / a
+        sel = (t - 64 < 56) & (t + 64 >= 71)
+        assert sel.sum() > 100
+        assert rel_l2(y[i][sel], ref[sel]).max() < TOL
+
+
+# ----------------------------------------------------------------------------- correct (both stages)
+def gpu_correct(dc, x, W, fs, fc, tec, alpha):
+    import torch
+    p = dc.Plan(x.shape[-1], fs, fc, taps=W)
+    t = to_dev(x)
+    y = torch.empty_like(t)
+    p.correct(t, y, tec, alpha)
+    xt = from_dev(t)
+    assert np.array_equal(xt, x)                  # x untouched
+    return from_dev(y)
+
+
+@pytest.mark.parametrize("variant", ["a", "b"])
+def test_correct_c1(dc, variant):
+    c = synth.c1_pulse(variant)
+    y = gpu_correct(dc, c["x"][None], c["W"], c["fs"], c["fc"], [c["tec"]], [c["alpha"]])
+    ref = O.run_batch("correct", c["x"][None], c["fs"], c["fc"], c["W"], [c["tec"]], [c["alpha"]])
+    assert rel_l2(y, ref).max() < TOL
+
+
+@pytest.mark.parametrize("log2n", [12, 16, 20])
+def test_correct_pulse_train_sampled(dc, log2n):
+    n = 1 << log2n
+    batch = 24 if log2n == 20 else 64
+    bank = synth.waveform_bank(n, count=8, T=min(100e-6, 0.4 * n / 2.048e9))
+    tec, alpha = synth.pulse_params(batch)
+    x = bank[np.arange(batch) % 8]
+    y = gpu_correct(dc, x, 32, 2.048e9, 0.0, tec, alpha)
+    idx = [0, 1, batch // 2, batch - 1]
+    ref = O.run_batch("correct", x[idx], 2.048e9, 0.0, 32, tec[idx], alpha[idx])
+    assert rel_l2(y[idx], ref).max() < TOL
+
+
+def test_correct_host_matches_device(dc):
+    import torch
+    n, batch = 1 << 14, 40
+    x = synth.complex_gaussian(n, seed=11, batch=batch).astype(np.complex64)
+    tec, alpha = synth.pulse_params(batch)
+    p = dc.Plan(n, 2.048e9, 0.0, taps=32)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    p.correct_host(xh, yh, tec, alpha)
+    yd = gpu_correct(dc, x, 32, 2.048e9, 0.0, tec, alpha)
+    assert np.array_equal(yh.numpy(), yd)
+    y_np = np.empty_like(x)
+    p.correct_host(x, y_np, tec, alpha)            # pageable numpy buffers too
+    assert np.array_equal(y_np, yd)
+
+
+# ----------------------------------------------------------------------------- errors through the ABI
+def test_abi_errors_on_gpu(dc):
+    import torch
+    p = dc.Plan(1024, 1e6, 0.0, taps=8)
+    x = torch.zeros(4, 1024, dtype=torch.complex64, device="cuda")
+    y = torch.zeros(4, 1024, dtype=torch.complex64, device="cuda")
+    with pytest.raises(dc.DispCorrError) as e:
+        p.iono(x, [1.0, -1.0, 0, 0])
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
+    with pytest.raises(dc.DispCorrError) as e:
+        p.doppler(x, y, [1.0, 0.0, 1, 1])
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
+    with pytest.raises(dc.DispCorrError) as e:
+        p.doppler(x, x, [1.0] * 4)
+    assert e.value.name == "DC_ERR_ALIASING"
+    flat = torch.zeros(4 * 1024 + 1, dtype=torch.complex64, device="cuda")
+    with pytest.raises(dc.DispCorrError) as e:
+        lib = dc.load()
+        import ctypes
+        arr = (ctypes.c_double * 1)(0.0)
+        st = lib.dc_iono(p._h, ctypes.c_void_p(flat.data_ptr() + 8), 1, arr)
+        dc._check(st)
+    assert e.value.name == "DC_ERR_MISALIGNED"
+    host = torch.zeros(1024, dtype=torch.complex64)
+    with pytest.raises(dc.DispCorrError) as e:
+        lib = dc.load()
+        import ctypes
+        arr = (ctypes.c_double * 1)(0.0)
+        dc._check(lib.dc_iono(p._h, ctypes.c_void_p(host.data_ptr()), 1, arr))
+    assert e.value.name == "DC_ERR_NOT_DEVICE_MEMORY"
+    p.sync()
+    info = p.info()
+    assert info["regime"] == 0 and info["n"] == 1024
