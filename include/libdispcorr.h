@@ -120,6 +120,21 @@ typedef struct {
 } dc_plan_info_t;
 dc_status dc_plan_info(dc_plan_t plan, dc_plan_info_t *info);
 
+/* Per-kernel-class timing (for the benchmark's roofline figures).  When enabled, every kernel
+ * the plan launches is bracketed by CUDA events on the plan's stream; dc_profile_read()
+ * synchronises the stream and returns, per class, the launches, summed device milliseconds and
+ * samples processed since the last reset.  Classes: DC_K_IONO_SMALL (regime-0 fused FFT ->
+ * phase -> IFFT), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler). */
+enum { DC_K_IONO_SMALL = 0, DC_K_FOURSTEP_A = 1, DC_K_FOURSTEP_B = 2, DC_K_FOURSTEP_C = 3, DC_K_DOPPLER = 4,
+       DC_K_CLASSES = 5 };
+typedef struct {
+  int64_t launches[DC_K_CLASSES];
+  double ms[DC_K_CLASSES];
+  int64_t samples[DC_K_CLASSES];
+} dc_profile_t;
+dc_status dc_profile_enable(dc_plan_t plan, int enable); /* also resets the counters */
+dc_status dc_profile_read(dc_plan_t plan, dc_profile_t *out);
+
 /* Human-readable name of a status code (static string). */
 const char *dc_status_string(dc_status s);
 

@@ -39,6 +39,13 @@ class DispCorrError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
+KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler")
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5), ("samples", ctypes.c_int64 * 5)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("log2n", ctypes.c_int), ("taps", ctypes.c_int), ("regime", ctypes.c_int),
                 ("n1", ctypes.c_int64), ("n2", ctypes.c_int64), ("chunk_pulses", ctypes.c_int64),
@@ -70,6 +77,8 @@ def load():
         "dc_correct": ([p, p, p, i64, pd, pd], i32),
         "dc_correct_host": ([p, p, p, i64, pd, pd], i32),
         "dc_plan_info": ([p, ctypes.POINTER(PlanInfo)], i32),
+        "dc_profile_enable": ([p, i32], i32),
+        "dc_profile_read": ([p, ctypes.POINTER(Profile)], i32),
         "dc_status_string": ([i32], ctypes.c_char_p),
         "dc_last_error_message": ([], ctypes.c_char_p),
         "dc_alpha_from_velocity": ([d], d),
@@ -180,6 +189,17 @@ class Plan:
         inf = PlanInfo()
         _check(load().dc_plan_info(self._h, ctypes.byref(inf)))
         return {f: getattr(inf, f) for f, _ in PlanInfo._fields_}
+
+    def profile_enable(self, on: bool = True):
+        """Bracket every kernel launch with CUDA events (resets the counters)."""
+        _check(load().dc_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """{class: {"launches", "ms", "samples"}} since the last profile_enable()."""
+        pr = Profile()
+        _check(load().dc_profile_read(self._h, ctypes.byref(pr)))
+        return {name: {"launches": pr.launches[i], "ms": pr.ms[i], "samples": pr.samples[i]}
+                for i, name in enumerate(KERNEL_CLASSES)}
 
     # -- hot path
     def iono(self, x, tec):

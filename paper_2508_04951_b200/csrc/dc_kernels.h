@@ -52,7 +52,8 @@ struct FourStepArgs {
   double fs_over_n, fc;
   cudaStream_t stream;
 };
-cudaError_t launch_iono_fourstep(const FourStepArgs &a, bool distort, int *launches);
+// pass 0 = A (columns, forward), 1 = B (rows, phase), 2 = C (columns, inverse)
+cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, bool distort);
 
 struct DopplerArgs {
   const float2 *x;
@@ -65,7 +66,7 @@ struct DopplerArgs {
   double carrier_cycles_per_sample;  // fc / fs; carrier phase psi_m = fc (1 - beta) m / fs
   cudaStream_t stream;
 };
-cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1, int *launches);
+cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
 int doppler_path(double max_abs_beta_m1);
 
 }  // namespace dc

@@ -77,6 +77,17 @@ struct dc_plan_s {
   ParamSlot ring[kRingSlots];
   int ring_next = 0;
   int64_t launches = 0;
+  // profiling (dc_profile_enable)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Rec {
+    int cls;
+    int64_t samples;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  dc_profile_t acc{};
 };
 
 namespace {
@@ -85,7 +96,7 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 // FP32 twiddle tables generated in binary64: section [NS][R], entry r = exp(-2 pi i k r / (NS R)).
 std::vector<float2> build_pass_tables(const dc::PlanDesc &d, bool inv) {
-  std::vector<float2> t((size_t)std::max(d.tw_size, 2));
+  std::vector<float2> t((size_t)std::max(d.tw_size, 2), make_float2(0.f, 0.f));
   for (int i = 0; i < d.npass; ++i) {
     const int lns = inv ? d.log_ns_inv[i] : d.log_ns_fwd[i];
     const int lr = inv ? d.log_radix_inv[i] : d.log_radix_fwd[i];
@@ -95,7 +106,7 @@ std::vector<float2> build_pass_tables(const dc::PlanDesc &d, bool inv) {
       for (int64_t r = 0; r < R; ++r) {
         const int64_t e = (k * r) % M;
         const double ang = -2.0 * dc::kPi * (double)e / (double)M;
-        t[(size_t)(off + k * R + r)] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        t.at((size_t)(off + k * R + r)) = make_float2((float)std::cos(ang), (float)std::sin(ang));
       }
   }
   return t;
@@ -194,14 +205,44 @@ dc_status release_slot(dc_plan_s *p, ParamSlot *s) {
   return DC_OK;
 }
 
+// ---- profiling brackets ----------------------------------------------------------------------------
+cudaEvent_t prof_event(dc_plan_s *p) {
+  if (p->ev_used == p->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    p->ev_pool.push_back(e);
+  }
+  return p->ev_pool[p->ev_used++];
+}
+
+struct ProfScope {
+  dc_plan_s *p;
+  int cls;
+  int64_t samples;
+  cudaEvent_t a = nullptr;
+  ProfScope(dc_plan_s *p_, int cls_, int64_t samples_) : p(p_), cls(cls_), samples(samples_) {
+    p->launches += 1;
+    if (p->prof && (a = prof_event(p))) cudaEventRecord(a, p->stream);
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(p);
+      if (b) {
+        cudaEventRecord(b, p->stream);
+        p->recs.push_back({cls, samples, a, b});
+      }
+    }
+  }
+};
+
 // ---- stage launchers (no validation) -----------------------------------------------------------
 dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                    int64_t pulse_base, bool distort) {
   if (p->regime == 0) {
     dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp + pulse_base, p->tw_small_f, p->tw_small_i,
                         p->fs / (double)p->n, p->fc, p->stream};
+    ProfScope ps(p, DC_K_IONO_SMALL, pulses * p->n);
     DC_CUDA(dc::launch_iono_small(a, distort), "iono_small_kernel launch");
-    p->launches += 1;
     return DC_OK;
   }
   dc::FourStepArgs a{};
@@ -222,18 +263,18 @@ dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses,
   a.fs_over_n = p->fs / (double)p->n;
   a.fc = p->fc;
   a.stream = p->stream;
-  int l = 0;
-  DC_CUDA(dc::launch_iono_fourstep(a, distort, &l), "four-step kernel launch");
-  p->launches += l;
+  for (int pass = 0; pass < 3; ++pass) {
+    ProfScope ps(p, DC_K_FOURSTEP_A + pass, pulses * p->n);
+    DC_CUDA(dc::launch_iono_fourstep_pass(a, pass, distort), "four-step kernel launch");
+  }
   return DC_OK;
 }
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                       int64_t pulse_base, double max_abs_beta_m1) {
   dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, p->stream};
-  int l = 0;
-  DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1, &l), "doppler kernel launch");
-  p->launches += l;
+  ProfScope ps(p, DC_K_DOPPLER, pulses * p->n);
+  DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
   return DC_OK;
 }
 
@@ -383,6 +424,7 @@ dc_status dc_plan_destroy(dc_plan_t p) {
     if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
     if (p->ev_out[i]) cudaEventDestroy(p->ev_out[i]);
   }
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
   if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
   delete p;
@@ -521,6 +563,40 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
   if ((s = release_slot(p, slot)) != DC_OK) return s;
   DC_CUDA(cudaStreamSynchronize(p->s_d2h), "cudaStreamSynchronize(D2H)");
   DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
+  return DC_OK;
+}
+
+static dc_status prof_collect(dc_plan_t p) {
+  if (p->recs.empty()) return DC_OK;
+  DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize(profile)");
+  for (auto &r : p->recs) {
+    float ms = 0.f;
+    DC_CUDA(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+    p->acc.launches[r.cls] += 1;
+    p->acc.ms[r.cls] += ms;
+    p->acc.samples[r.cls] += r.samples;
+  }
+  p->recs.clear();
+  p->ev_used = 0;
+  return DC_OK;
+}
+
+dc_status dc_profile_enable(dc_plan_t p, int enable) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize(profile)");
+  p->recs.clear();
+  p->ev_used = 0;
+  p->acc = dc_profile_t{};
+  p->prof = enable != 0;
+  return DC_OK;
+}
+
+dc_status dc_profile_read(dc_plan_t p, dc_profile_t *out) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  if (!out) return fail(DC_ERR_NULL_POINTER, "out is NULL");
+  dc_status s = prof_collect(p);
+  if (s != DC_OK) return s;
+  *out = p->acc;
   return DC_OK;
 }
 

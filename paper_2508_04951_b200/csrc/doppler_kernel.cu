@@ -270,8 +270,7 @@ int doppler_path(double max_abs_beta_m1) {
   return 0;
 }
 
-cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1, int *launches) {
-  if (launches) *launches += 1;
+cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1) {
   const int path = doppler_path(max_abs_beta_m1);
   if (path == 0) return launch_doppler_exact(a);
   return launch_doppler_fast(a, path == 2);

@@ -234,7 +234,9 @@ struct PassPlan {
     for (int q = 0; q < i; ++q) s += (1 << log_ns_inv(q)) << log_radix_inv(q);
     return s;
   }
-  __host__ __device__ static constexpr int tw_size() { return tw_off_fwd(npass); }
+  __host__ __device__ static constexpr int tw_size() {
+    return tw_off_fwd(npass) > tw_off_inv(npass) ? tw_off_fwd(npass) : tw_off_inv(npass);
+  }
 };
 
 // ----------------------------------------------------------------------------- tiles

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(Tile<P1, 32, C, false>::T)
         val = cmul(val, outer_tw((row * t2) & nmask, H, twh, twl));
         __stcg(a, val);
       } else {
-        __stcs(a, val);
+        __stcg(a, val);  // dc_correct reads it back from L2 (Doppler stage)
       }
     }
   }
@@ -391,16 +391,15 @@ void fourstep_split(int log2n, int &P1, int &P2) {
   P1 = log2n - P2;
 }
 
-cudaError_t launch_iono_fourstep(const FourStepArgs &a, bool distort, int *launches) {
+cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, bool distort) {
   int P1, P2;
   fourstep_split(a.log2n, P1, P2);
-  cudaError_t e = launch_col<false>(P1, a, a.src, a.dst);
-  if (e != cudaSuccess) return e;
-  e = distort ? launch_row<true>(P2, a) : launch_row<false>(P2, a);
-  if (e != cudaSuccess) return e;
-  e = launch_col<true>(P1, a, a.dst, a.dst);
-  if (launches) *launches += 3;
-  return e;
+  switch (pass) {
+    case 0: return launch_col<false>(P1, a, a.src, a.dst);
+    case 1: return distort ? launch_row<true>(P2, a) : launch_row<false>(P2, a);
+    case 2: return launch_col<true>(P1, a, a.dst, a.dst);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace dc

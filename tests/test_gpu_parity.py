@@ -47,7 +47,7 @@ def rel_l2(a, b):
 
 
 def gpu_iono(dc, x, fs, fc, tec, distort=False):
-    p = dc.Plan(x.shape[-1], fs, fc, taps=8)
+    p = dc.Plan(x.shape[-1], fs, fc, taps=min(8, x.shape[-1]))
     t = to_dev(x)
     (p.iono_distort if distort else p.iono)(t, tec)
     return from_dev(t)
