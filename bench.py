@@ -203,7 +203,8 @@ def main():
 
     pulses, log2n, taps, desc = CONFIGS[args.config]
     n = 1 << log2n
-    lo, hi = rank * pulses // ws, (rank + 1) * pulses // ws
+    from paper_2508_04951_b200.dist import max_over_ranks, shard_range
+    lo, hi = shard_range(pulses, rank, ws)
     my = hi - lo
     bank = synth.waveform_bank(n, count=16)
     index = np.arange(pulses) % 16
@@ -238,11 +239,7 @@ def main():
         if ws > 1:
             dist.barrier()
         launches = plan.info()["kernel_launches"] - l0
-    ms = ev0.elapsed_time(ev1)
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
     value = pulses * n * args.steps / (ms / 1e3)
     clocks = clk.summary()
 
@@ -291,11 +288,7 @@ def main():
         for _ in range(args.e2e_steps):
             plan.correct_host(xh, yh, tec_r, alpha_r)
         torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if ws > 1:
-            t = torch.tensor([el], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = max_over_ranks(time.perf_counter() - t0, device="cuda")
         e2e = {"value": pulses * n * args.e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(xh.numel() * 8 * ws), "d2h_bytes_per_step": int(yh.numel() * 8 * ws),
                "steps": args.e2e_steps, "api": "dc_correct_host (pinned host buffers, chunked H2D/compute/D2H overlap)"}

@@ -22,7 +22,8 @@ import numpy as np
 __all__ = ["Plan", "DispCorrError", "alpha_from_velocity", "k2_per_tec", "library_path", "load", "STATUS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libdispcorr.so")
+# DISPCORR_LIB selects an alternative in-tree build (kernel tuning variants, tools/debug/)
+_LIB_PATH = os.environ.get("DISPCORR_LIB", os.path.join(_HERE, "lib", "libdispcorr.so"))
 _lib = None
 
 STATUS = {

@@ -24,6 +24,8 @@
 //     With |delta| <= 2e-3 the truncation error is < 2e-9 (second order), far inside 1e-5.
 //   * The slow path (|beta - 1| too large for the union/Taylor scheme) evaluates every
 //     output directly (Alg. 1 structure).
+#include <algorithm>
+
 #include "dc_kernels.h"
 
 namespace dc {
@@ -80,120 +82,218 @@ __device__ __forceinline__ TapW tap_weight(float u, int m, float S, float Cc, bo
   return t;
 }
 
+// async 8-byte global -> shared copy with zero fill when `valid` is false (cp.async, LDGSTS)
+__device__ __forceinline__ void cp_async8(float2 *smem_dst, const float2 *gsrc, bool valid) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int src_size = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(src_size) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+struct DopTile {
+  int64_t pulse, m0, Bcta;
+  double beta;
+  int span;
+};
+
+__device__ __forceinline__ DopTile dop_tile(int64_t item, int64_t tiles_per_pulse, int64_t n, int W,
+                                            const PulseParams *__restrict__ pp, int64_t pulse_base) {
+  DopTile t;
+  t.pulse = item / tiles_per_pulse;
+  t.m0 = (item - t.pulse * tiles_per_pulse) * kDopM;
+  t.beta = pp[pulse_base + t.pulse].beta;
+  const double halfW = 0.5 * (double)W;
+  const int lo_shift = (t.beta < 1.0) ? 1 : 0;
+  t.Bcta = (int64_t)floor((double)t.m0 * t.beta - halfW) + 1 - lo_shift;
+  const int64_t mlast = t.m0 + kDopM - 1;
+  const int64_t Kend = (int64_t)floor((double)mlast * t.beta - halfW) + 1 + W + 2 * kDopR + 8;
+  t.span = (int)(Kend - t.Bcta);
+  return t;
+}
+
+// stage x[Bcta, Bcta + span) of the tile's pulse into padded shared memory (zeros outside [0, n))
+__device__ __forceinline__ void dop_stage(float2 *buf, const DopTile &t, const float2 *__restrict__ x, int64_t n) {
+  const float2 *xp = x + t.pulse * n;
+  for (int i = threadIdx.x; i < t.span; i += kDopT) {
+    const int64_t k = t.Bcta + i;
+    const bool ok = (k >= 0 && k < n);
+    cp_async8(buf + dpad(i), xp + (ok ? k : 0), ok);
+  }
+}
+
+// Persistent, double-buffered pipeline: while the CTA computes tile i from one shared buffer,
+// the input span of tile i + gridDim.x streams into the other with cp.async (zero-filled).
 template <bool SECOND>
-__global__ void __launch_bounds__(kDopT) doppler_fast_kernel(const float2 *__restrict__ x, float2 *__restrict__ y,
-                                                            int64_t n, int W, const PulseParams *__restrict__ pp,
-                                                            int64_t pulse_base, double carrier) {
+__global__ void __launch_bounds__(kDopT, 2)
+    doppler_pipe_kernel(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t n, int W,
+                        const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
+                        int buf_elems) {
   extern __shared__ float2 xs[];
   const int tid = threadIdx.x;
-  const int64_t pulse = blockIdx.y;
-  const float2 *xp = x + pulse * n;
-  float2 *yp = y + pulse * n;
-  const double beta = pp[pulse_base + pulse].beta;
+  const int64_t tiles_per_pulse = (n + kDopM - 1) / kDopM;
+  const int64_t total = pulses * tiles_per_pulse;
   const double halfW = 0.5 * (double)W;
-  const int64_t m0 = (int64_t)blockIdx.x * kDopM;
-  if (m0 >= n) return;
-  // union base of output r of a thread whose first output is mt: B + r with
-  // B = K(mt) - 1 if beta < 1 (a window may start one sample early), else K(mt).
-  const int lo_shift = (beta < 1.0) ? 1 : 0;
-  const double tc0 = (double)m0 * beta;
-  const int64_t Bcta = (int64_t)floor(tc0 - halfW) + 1 - lo_shift;
-  const int64_t mlast = min(m0 + kDopM, n) - 1;
-  const int64_t Kend = (int64_t)floor((double)mlast * beta - halfW) + 1 + W + 1;  // exclusive, with slack
-  const int span = (int)(Kend - Bcta);
+  int64_t item = blockIdx.x;
+  if (item >= total) return;
+  DopTile cur = dop_tile(item, tiles_per_pulse, n, W, pp, pulse_base);
+  dop_stage(xs, cur, x, n);
+  cp_async_commit();
+  int bsel = 0;
+  for (; item < total; item += gridDim.x) {
+    // ---- prefetch the next tile into the other buffer
+    const int64_t nitem = item + gridDim.x;
+    DopTile nxt;
+    if (nitem < total) {
+      nxt = dop_tile(nitem, tiles_per_pulse, n, W, pp, pulse_base);
+      dop_stage(xs + (bsel ^ 1) * buf_elems, nxt, x, n);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const float2 *sb = xs + bsel * buf_elems;
 
-  // ---- stage the input span (zero outside [0, n)) into padded shared memory
-  for (int i = tid; i < span; i += kDopT) {
-    const int64_t k = Bcta + i;
-    xs[dpad(i)] = (k >= 0 && k < n) ? __ldcs(xp + k) : make_float2(0.f, 0.f);
-  }
-  __syncthreads();
-
-  const int64_t mt = m0 + (int64_t)tid * kDopR;
-  if (mt >= n) return;
-  const int nout = (int)min((int64_t)kDopR, n - mt);
-
-  // ---- exact binary64 window bookkeeping per output
-  const double t0 = (double)mt * beta;
-  const int64_t B = (int64_t)floor(t0 - halfW) + 1 - lo_shift;
-  float mask0[kDopR], maskW[kDopR], delta[kDopR];
-  constexpr int rref = kDopR / 2;
-  const double tref = (double)(mt + rref) * beta;
-  const double vref = tref - (double)(B + rref);  // continuous position inside the union (~W/2)
+    // ---- this thread's R consecutive outputs
+    const int64_t mt = cur.m0 + (int64_t)tid * kDopR;
+    const double beta = cur.beta;
+    const int lo_shift = (beta < 1.0) ? 1 : 0;
+    const int64_t B = (int64_t)floor((double)mt * beta - halfW) + 1 - lo_shift;
+    float mask0[kDopR], maskW[kDopR];
 #pragma unroll
-  for (int r = 0; r < kDopR; ++r) {
-    const double tr = (double)(mt + r) * beta;
-    const int64_t Kr = (int64_t)floor(tr - halfW) + 1;
-    const int a = (int)(Kr - r - B);  // 0 or 1: offset of this output's window inside the union
-    mask0[r] = (a == 0) ? 1.f : 0.f;
-    maskW[r] = (a == 1) ? 1.f : 0.f;
-    delta[r] = __double2float_rn((tr - (double)(B + r)) - vref);
-  }
-  // reference position split into nearest integer + fraction in [-1/2, 1/2]
-  const double ic_d = rint(vref);
-  const int ic = (int)ic_d;
-  const float u = __double2float_rn(vref - ic_d);
-  float S, Cc;
-  sincospif(u, &S, &Cc);
-  S *= 0.31830988618379067f;  // sin(pi u) / pi
-
-  float2 acc[kDopR];
+    for (int r = 0; r < kDopR; ++r) {
+      const int64_t Kr = (int64_t)floor((double)(mt + r) * beta - halfW) + 1;
+      const int a = (int)(Kr - r - B);  // 0 or 1: this output's window offset inside the union
+      mask0[r] = (a == 0) ? 1.f : 0.f;
+      maskW[r] = (a == 1) ? 1.f : 0.f;
+    }
+    // Taylor steps delta_r = (r - R/2)(beta - 1), paired for FFMA2
+    const float db = (float)(beta - 1.0);
+    float2 dl[kDopR / 2];
 #pragma unroll
-  for (int r = 0; r < kDopR; ++r) acc[r] = make_float2(0.f, 0.f);
-
-  const int lb = (int)(B - Bcta);  // thread base inside the staged span
-  // register window: win[i] = x[B + jj0 + i]
-  float2 win[2 * kDopR];
-#pragma unroll
-  for (int i = 0; i < kDopR; ++i) win[i] = xs[dpad(lb + i)];
-
-  // taps jj = 0 .. W (W + 1 union taps), streamed in chunks of R
-  int jj0 = 0;
-  const int ntaps = W + 1;
-  for (; jj0 < ntaps; jj0 += kDopR) {
-#pragma unroll
-    for (int i = 0; i < kDopR; ++i) win[kDopR + i] = xs[dpad(lb + jj0 + kDopR + i)];
-#pragma unroll
-    for (int q = 0; q < kDopR; ++q) {
-      const int jj = jj0 + q;
-      if (jj < ntaps) {
-        TapW tw = tap_weight(u, jj - ic, S, Cc, SECOND);
-        const bool e0 = (jj == 0), eW = (jj == W);
-#pragma unroll
-        for (int r = 0; r < kDopR; ++r) {
-          float h = SECOND ? fmaf(fmaf(0.5f * tw.w2, delta[r], tw.w1), delta[r], tw.w) : fmaf(tw.w1, delta[r], tw.w);
-          if (e0) h *= mask0[r];
-          if (eW) h *= maskW[r];
-          const float2 xv = win[q + r];
-          acc[r].x = fmaf(xv.x, h, acc[r].x);
-          acc[r].y = fmaf(xv.y, h, acc[r].y);
-        }
+    for (int h = 0; h < kDopR / 2; ++h) dl[h] = make_float2((2 * h - kDopR / 2) * db, (2 * h + 1 - kDopR / 2) * db);
+    // reference position inside the union, split into nearest integer + fraction in [-1/2, 1/2]
+    const double vref = (double)(mt + kDopR / 2) * beta - (double)(B + kDopR / 2);
+    const double ic_d = rint(vref);
+    const int ic = (int)ic_d;
+    const float u = __double2float_rn(vref - ic_d);
+    float S, Cc;
+    sincospif(u, &S, &Cc);
+    S *= 0.31830988618379067f;  // sin(pi u) / pi
+    // centre-tap weights (d = u): series near 0 (sinc even; avoids C/d - S/(pi d^2) cancellation)
+    float wc, w1c, w2c;
+    {
+      const float pd2 = 9.8696044010893586f * u * u;
+      if (fabsf(u) < 0.25f) {
+        wc = (u == 0.f) ? 1.f : S * frcp(u);
+        w1c = -3.2898681336964529f * u * (1.f - pd2 * (0.1f - pd2 * (1.f / 280.f)));
+        w2c = -3.2898681336964529f * (1.f - pd2 * (0.3f - pd2 * (1.f / 56.f)));
+      } else {
+        const float inv = frcp(u);
+        wc = S * inv;
+        w1c = inv * fmaf(-S, inv, Cc);
+        w2c = fmaf(-9.8696044010893586f, wc, -2.f * w1c * inv);
       }
     }
+    const int lb = (int)(B - cur.Bcta);
+    float2 acc[kDopR];
 #pragma unroll
-    for (int i = 0; i < kDopR; ++i) win[i] = win[kDopR + i];
-  }
+    for (int r = 0; r < kDopR; ++r) acc[r] = make_float2(0.f, 0.f);
 
-  // ---- carrier rotation exp(-i 2 pi fc (1 - beta) m / fs) (reading R10), phase reduced in binary64
-  const double g = carrier * (1.0 - beta);
-  float2 out[kDopR];
+    // weights of union tap jj (d = u - (jj - ic)); returns (w, w1, w2)
+    auto weight = [&](int jj, float &w, float &w1, float &w2) {
+      const int m = jj - ic;
+      const float d = u - (float)m;
+      const float inv = frcp(d);
+      const float sg = (m & 1) ? -1.f : 1.f;
+      const float s = sg * S, c = sg * Cc;
+      w = s * inv;
+      w1 = inv * fmaf(-s, inv, c);
+      w2 = SECOND ? fmaf(-9.8696044010893586f, w, -2.f * w1 * inv) : 0.f;
+      if (m == 0) {
+        w = wc;
+        w1 = w1c;
+        w2 = w2c;
+      }
+    };
+    auto mac_tap = [&](const float2 *xv, float w, float w1, float w2, const float *mask) {
 #pragma unroll
-  for (int r = 0; r < kDopR; ++r) {
-    float2 v = acc[r];
-    if (g != 0.0) {
-      const double psi = g * (double)(mt + r);
-      const float rr = __double2float_rn(psi - rint(psi));
-      v = cmul(v, expm2pi(rr));
+      for (int h = 0; h < kDopR / 2; ++h) {
+        float2 hh;
+        if (SECOND) {
+          float2 t = __ffma2_rn(make_float2(0.5f * w2, 0.5f * w2), dl[h], make_float2(w1, w1));
+          hh = __ffma2_rn(t, dl[h], make_float2(w, w));
+        } else {
+          hh = __ffma2_rn(make_float2(w1, w1), dl[h], make_float2(w, w));
+        }
+        if (mask) {
+          hh.x *= mask[2 * h];
+          hh.y *= mask[2 * h + 1];
+        }
+        acc[2 * h] = __ffma2_rn(xv[2 * h], make_float2(hh.x, hh.x), acc[2 * h]);
+        acc[2 * h + 1] = __ffma2_rn(xv[2 * h + 1], make_float2(hh.y, hh.y), acc[2 * h + 1]);
+      }
+    };
+
+    {  // edge tap jj = 0 (owned by outputs with a_r == 0)
+      float2 xv[kDopR];
+#pragma unroll
+      for (int r = 0; r < kDopR; ++r) xv[r] = sb[dpad(lb + r)];
+      float w, w1, w2;
+      weight(0, w, w1, w2);
+      mac_tap(xv, w, w1, w2, mask0);
     }
-    out[r] = v;
-  }
-  if (nout == kDopR) {
-    float4 *y4 = reinterpret_cast<float4 *>(yp + mt);
+    // interior taps jj = 1 .. W-1, streamed in chunks of R through a register window
+    float2 win[2 * kDopR];
 #pragma unroll
-    for (int h = 0; h < kDopR / 2; ++h) __stcs(y4 + h, make_float4(out[2 * h].x, out[2 * h].y, out[2 * h + 1].x, out[2 * h + 1].y));
-  } else {
-    for (int r = 0; r < nout; ++r) yp[mt + r] = out[r];
+    for (int i = 0; i < kDopR; ++i) win[i] = sb[dpad(lb + 1 + i)];
+    for (int jj0 = 1; jj0 < W; jj0 += kDopR) {
+#pragma unroll
+      for (int i = 0; i < kDopR; ++i) win[kDopR + i] = sb[dpad(lb + jj0 + kDopR + i)];
+#pragma unroll
+      for (int q = 0; q < kDopR; ++q) {
+        float w, w1, w2;
+        weight(jj0 + q, w, w1, w2);
+        if (jj0 + q >= W) w = w1 = w2 = 0.f;  // padding taps of the last chunk
+        mac_tap(&win[q], w, w1, w2, nullptr);
+      }
+#pragma unroll
+      for (int i = 0; i < kDopR; ++i) win[i] = win[kDopR + i];
+    }
+    {  // edge tap jj = W (owned by outputs with a_r == 1)
+      float2 xv[kDopR];
+#pragma unroll
+      for (int r = 0; r < kDopR; ++r) xv[r] = sb[dpad(lb + r + W)];
+      float w, w1, w2;
+      weight(W, w, w1, w2);
+      mac_tap(xv, w, w1, w2, maskW);
+    }
+
+    // ---- carrier rotation (reading R10) and store
+    const double g = carrier * (1.0 - beta);
+    float2 *yp = y + cur.pulse * n;
+    if (g != 0.0) {
+#pragma unroll
+      for (int r = 0; r < kDopR; ++r) {
+        const double psi = g * (double)(mt + r);
+        acc[r] = cmul(acc[r], expm2pi(__double2float_rn(psi - rint(psi))));
+      }
+    }
+    if (mt + kDopR <= n) {
+      float4 *y4 = reinterpret_cast<float4 *>(yp + mt);
+#pragma unroll
+      for (int h = 0; h < kDopR / 2; ++h)
+        __stcs(y4 + h, make_float4(acc[2 * h].x, acc[2 * h].y, acc[2 * h + 1].x, acc[2 * h + 1].y));
+    } else {
+#pragma unroll
+      for (int r = 0; r < kDopR; ++r)
+        if (mt + r < n) yp[mt + r] = acc[r];
+    }
+    __syncthreads();  // everyone is done with buffer bsel before it is refilled
+    cur = nxt;
+    bsel ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 // Exact-tap, one-output-per-thread path (Alg. 1 structure) for any alpha.
@@ -240,15 +340,21 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
 }
 
 static cudaError_t launch_doppler_fast(const DopplerArgs &a, bool second) {
-  const int64_t tiles = (a.n + kDopM - 1) / kDopM;
-  // staged span <= M * max(beta) + W + 3, plus the register window's read-ahead (2R)
-  const int span = (int)(kDopM * (1.0 + 2.0 * kDopMaxDrift)) + a.taps + 3 * kDopR + 8;
-  const size_t smem = sizeof(float2) * (size_t)(span + (span >> 3) + 8);
-  auto kern = second ? doppler_fast_kernel<true> : doppler_fast_kernel<false>;
+  const int64_t tiles = (a.n + kDopM - 1) / kDopM * a.pulses;
+  // staged span <= M * max(beta) + W + 2R + 10 samples (fast path: |beta - 1| <= 5e-4), padded 9/8
+  const int span = (int)(kDopM * (1.0 + 2.0 * kDopMaxDrift)) + a.taps + 2 * kDopR + 16;
+  const int buf = span + (span >> 3) + 8;
+  const size_t smem = 2 * sizeof(float2) * (size_t)buf;
+  auto kern = second ? doppler_pipe_kernel<true> : doppler_pipe_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)tiles, (unsigned)a.pulses);
-  kern<<<grid, kDopT, smem, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample);
+  int dev = 0, sms = 148, per_sm = 2;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDopT, smem);
+  const int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, kDopT, smem, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample,
+                                                  a.pulses, buf);
   return cudaGetLastError();
 }
 

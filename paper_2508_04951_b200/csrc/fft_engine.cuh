@@ -312,7 +312,7 @@ __device__ __forceinline__ void pass_compute(float2 (&v)[TL::E], int tid, const 
       if constexpr (R >= 2) {
 #pragma unroll
         for (int h = 0; h < R / 2; ++h) {
-          float4 p = __ldg(t4 + h);
+          float4 p = t4[h];  // shared-memory or L1-cached global table
           w[2 * h] = make_float2(p.x, p.y);
           w[2 * h + 1] = make_float2(p.z, p.w);
         }

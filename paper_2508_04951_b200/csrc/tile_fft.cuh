@@ -1,0 +1,255 @@
+// tile_fft.cuh -- persistent, prefetching tile kernels for the ionospheric stage (Eq. 15).
+//
+// Every regime is expressed as a stream of 8192-sample TILES, each processed by one CTA:
+//   SMALL  rows = whole pulses (n <= 8192): forward FFT -> Eq. 15 phase -> inverse FFT
+//   COLA   four-step pass A: [N1][C] column tile, forward N1-point DFTs, times w_n^(k1 t2)
+//   ROWB   four-step pass B: [NB][N2] row tile, forward DFT -> phase -> inverse DFT, times w_n^(-k1 t2)
+//   COLC   four-step pass C: [N1][C] column tile, inverse N1-point DFTs
+// A CTA is persistent: while it computes tile i, the input of tile i + gridDim.x streams
+// into a shared-memory staging buffer with cp.async (16-byte LDGSTS, L1-bypassing), so the
+// HBM/L2 latency of the next tile overlaps this tile's FFT passes.  Twiddle tables are copied
+// into shared memory once per CTA.  The first FFT pass reads the staging buffer, the
+// exchanges between passes use a separate padded work buffer, the last pass stores straight
+// from registers to global memory.
+#pragma once
+#include "fft_engine.cuh"
+
+namespace dc {
+
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16_zfill(void *smem_dst, const void *gsrc, bool valid) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+enum TileMode { MODE_SMALL = 0, MODE_COLA = 1, MODE_ROWB = 2, MODE_COLC = 3 };
+
+struct TileArgs {
+  const float2 *src;  // tile input (pulse-major, pulse_stride apart)
+  float2 *dst;        // tile output
+  int64_t pulses;     // pulses in this launch
+  int64_t pulse_stride;
+  int64_t pulse_base;  // first pulse's index in pp[]
+  int log2n;
+  const PulseParams *pp;
+  const float2 *twf, *twi;  // pass tables of the tile's FFT size (global; copied to smem)
+  const float2 *twh, *twl;  // four-step outer twiddles (global; copied to smem)
+  int H;
+  double fs_over_n, fc;
+};
+
+// Shared-memory layout (float2 units): [staging ELEMS][work SMEM_ELEMS][twf][twi][twh][twl]
+template <int P, int LOGE, int NB, bool ROW, int MODE>
+struct TileCfg {
+  using TL = Tile<P, (1 << LOGE), NB, ROW>;
+  using PP = PassPlan<P, LOGE>;
+  static constexpr int L = 1 << P;
+  static constexpr int T = TL::T;
+  // pass tables live in shared memory when small (four-step sizes); the regime-0 tables of
+  // large pulses (~L entries per direction) stay in global memory (L1-cached)
+  static constexpr int TWF_ALL = (MODE == MODE_COLC) ? 0 : PP::tw_off_fwd(PP::npass);
+  static constexpr int TWI_ALL = (MODE == MODE_COLA) ? 0 : PP::tw_off_inv(PP::npass);
+  static constexpr bool SMEM_TW = (TWF_ALL + TWI_ALL) * 8 <= 40 * 1024;
+  static constexpr int TWF = SMEM_TW ? TWF_ALL : 0;
+  static constexpr int TWI = SMEM_TW ? TWI_ALL : 0;
+  static constexpr int TWF_PAD = (TWF + 1) & ~1;
+  static constexpr int TWI_PAD = (TWI + 1) & ~1;
+  static __host__ __device__ constexpr int outer_elems(int H, int log2n) {
+    return (MODE == MODE_COLA || MODE == MODE_ROWB) ? ((1 << H) + (1 << (log2n - H))) : 0;
+  }
+  static __host__ __device__ constexpr size_t smem_bytes(int H, int log2n) {
+    return sizeof(float2) * ((size_t)TL::ELEMS + TL::SMEM_ELEMS + TWF_PAD + TWI_PAD + outer_elems(H, log2n));
+  }
+};
+
+template <int P, int LOGE, int NB, bool ROW, int MODE, bool DISTORT>
+__global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_fft_kernel(const TileArgs a) {
+  using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
+  using TL = typename CFG::TL;
+  using PP = typename CFG::PP;
+  constexpr int L = CFG::L;
+  constexpr int E = 1 << LOGE;
+  constexpr int T = CFG::T;
+  constexpr int NP = PP::npass;
+  constexpr bool FWD = (MODE != MODE_COLC);
+  constexpr bool INVP = (MODE != MODE_COLA);
+  constexpr int R0 = 1 << (FWD ? PP::log_radix_fwd(0) : PP::log_radix_inv(0));
+  extern __shared__ float4 smem4[];
+  float2 *S = reinterpret_cast<float2 *>(smem4);
+  float2 *Wk = S + TL::ELEMS;
+  float2 *Tf = Wk + TL::SMEM_ELEMS;
+  float2 *Ti = Tf + CFG::TWF_PAD;
+  float2 *Th = Ti + CFG::TWI_PAD;
+  const int H = a.H;
+  float2 *Tl = Th + ((MODE == MODE_COLA || MODE == MODE_ROWB) ? (1 << (a.log2n - H)) : 0);
+  const int tid = threadIdx.x;
+
+  // ---- geometry of the tile stream
+  const int log2n = a.log2n;
+  const int n = 1 << log2n;
+  int64_t tiles_per_pulse;
+  int n2 = 0;
+  if constexpr (MODE == MODE_SMALL) {
+    tiles_per_pulse = 1;  // (NB pulses per tile; see below)
+  } else if constexpr (ROW) {
+    tiles_per_pulse = (n >> P) / NB;  // rows k1 of N2 = L samples, NB per tile
+  } else {
+    n2 = n >> P;
+    tiles_per_pulse = n2 / NB;  // column groups of NB columns
+  }
+  const int64_t total = (MODE == MODE_SMALL) ? (a.pulses + NB - 1) / NB : a.pulses * tiles_per_pulse;
+  int64_t item = blockIdx.x;
+  if (item >= total) return;
+
+  // staging: issue the cp.async for tile `it` into S
+  auto stage = [&](int64_t it) {
+    if constexpr (MODE == MODE_SMALL) {
+      const int64_t p0 = it * NB;
+      const int64_t valid = min((int64_t)NB, a.pulses - p0) * L;  // samples of real pulses in the tile
+      const float4 *g = reinterpret_cast<const float4 *>(a.src + p0 * L);
+      float4 *s4 = reinterpret_cast<float4 *>(S);
+      for (int i = tid; i < TL::ELEMS / 2; i += T) {
+        const bool ok = 2 * (int64_t)i < valid;
+        cp_async16_zfill(s4 + i, ok ? (const void *)(g + i) : (const void *)a.src, ok);
+      }
+    } else if constexpr (ROW) {
+      const int64_t pulse = it / tiles_per_pulse;
+      const int64_t r0 = (it - pulse * tiles_per_pulse) * NB;
+      const float4 *g = reinterpret_cast<const float4 *>(a.src + pulse * a.pulse_stride + r0 * L);
+      float4 *s4 = reinterpret_cast<float4 *>(S);
+#pragma unroll 4
+      for (int i = tid; i < TL::ELEMS / 2; i += T) cp_async16(s4 + i, g + i);
+    } else {
+      const int64_t pulse = it / tiles_per_pulse;
+      const int64_t c0 = (it - pulse * tiles_per_pulse) * NB;
+      const float2 *g = a.src + pulse * a.pulse_stride + c0;
+      constexpr int V = NB / 2;  // float4 per row segment
+      float4 *s4 = reinterpret_cast<float4 *>(S);
+#pragma unroll 4
+      for (int i = tid; i < L * V; i += T) {
+        const int row = i / V, v = i - row * V;
+        cp_async16(s4 + i, reinterpret_cast<const float4 *>(g + (int64_t)row * n2) + v);
+      }
+    }
+  };
+  stage(item);
+  cp_async_commit_();
+
+  // ---- tables into shared memory (once)
+  for (int i = tid; i < CFG::TWF; i += T) Tf[i] = a.twf[i];
+  for (int i = tid; i < CFG::TWI; i += T) Ti[i] = a.twi[i];
+  if constexpr (MODE == MODE_COLA || MODE == MODE_ROWB) {
+    for (int i = tid; i < (n >> H); i += T) Th[i] = a.twh[i];
+    for (int i = tid; i < (1 << H); i += T) Tl[i] = a.twl[i];
+  }
+  const uint32_t nmask = (uint32_t)n - 1u;
+  const uint32_t hmask = (1u << H) - 1u;
+
+  for (; item < total; item += gridDim.x) {
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- first pass inputs from the staging buffer
+    float2 v[E];
+#pragma unroll
+    for (int q = 0; q < E / R0; ++q) {
+      int b, j;
+      TL::template bmap<R0>(tid + q * T, b, j);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + r * (L / R0);
+        v[q * R0 + r] = ROW ? S[b * L + i] : S[i * NB + b];
+      }
+    }
+    __syncthreads();  // staging buffer free: prefetch the next tile
+    const int64_t nitem = item + gridDim.x;
+    if (nitem < total) stage(nitem);
+    cp_async_commit_();
+
+    int64_t pulse, base;  // pulse of the tile; first row / column / pulse index
+    if constexpr (MODE == MODE_SMALL) {
+      pulse = item * NB;
+      base = 0;
+    } else {
+      pulse = item / tiles_per_pulse;
+      base = (item - pulse * tiles_per_pulse) * NB;
+    }
+
+    if constexpr (FWD) run_passes<TL, PP, 0, NP - 1, false>(v, Wk, tid, CFG::SMEM_TW ? Tf : a.twf);
+
+    if constexpr (MODE == MODE_SMALL || MODE == MODE_ROWB) {
+      // ---- frequency domain (Eq. 15): registers hold bins k2 = j + r L/RL of FFT b
+      constexpr int RL = 1 << PP::log_radix_fwd(NP - 1);
+      const float inv_n = 1.0f / (float)n;
+      const int P1 = log2n - P;
+#pragma unroll
+      for (int q = 0; q < E / RL; ++q) {
+        int b, j;
+        TL::template bmap<RL>(tid + q * T, b, j);
+        int64_t p;
+        int k1 = 0;
+        if constexpr (MODE == MODE_SMALL) {
+          p = pulse + b;
+        } else {
+          p = pulse;
+          k1 = (int)base + b;
+        }
+        const double nu_coef = (p < a.pulses) ? a.pp[a.pulse_base + p].nu_coef : 0.0;
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int k2 = j + r * (L / RL);
+          const int k = (MODE == MODE_SMALL) ? k2 : (k1 + (k2 << P1));
+          const int kk = (k >= n / 2) ? k - n : k;
+          const double f = a.fc + a.fs_over_n * (double)kk;
+          float2 m = make_float2(inv_n, 0.f);
+          if (f > 0.0 && nu_coef != 0.0) {
+            const double nu = nu_coef * drcp(f);
+            const float rf = __double2float_rn(nu - rint(nu));
+            const float2 w = expm2pi(DISTORT ? -rf : rf);
+            m = make_float2(w.x * inv_n, w.y * inv_n);
+          }
+          v[q * RL + r] = cmul(v[q * RL + r], m);
+        }
+      }
+    }
+
+    if constexpr (INVP) run_passes<TL, PP, 0, NP - 1, true>(v, Wk, tid, CFG::SMEM_TW ? Ti : a.twi);
+
+    // ---- last pass outputs straight to global memory
+    constexpr int RO = 1 << (INVP ? PP::log_radix_inv(NP - 1) : PP::log_radix_fwd(NP - 1));
+#pragma unroll
+    for (int q = 0; q < E / RO; ++q) {
+      int b, j;
+      TL::template bmap<RO>(tid + q * T, b, j);
+#pragma unroll
+      for (int r = 0; r < RO; ++r) {
+        const int i = j + r * (L / RO);  // output index within FFT b
+        float2 val = v[q * RO + r];
+        if constexpr (MODE == MODE_SMALL) {
+          const int64_t p = pulse + b;
+          if (p < a.pulses) __stcs(a.dst + p * L + i, val);
+        } else if constexpr (MODE == MODE_ROWB) {
+          const uint32_t k1 = (uint32_t)base + b;
+          const uint32_t m = (k1 * (uint32_t)i) & nmask;
+          val = cmulc(val, cmul(Th[m >> H], Tl[m & hmask]));
+          __stcg(a.dst + pulse * a.pulse_stride + (int64_t)k1 * L + i, val);
+        } else if constexpr (MODE == MODE_COLA) {
+          const uint32_t t2 = (uint32_t)base + b;
+          const uint32_t m = ((uint32_t)i * t2) & nmask;
+          val = cmul(val, cmul(Th[m >> H], Tl[m & hmask]));
+          __stcg(a.dst + pulse * a.pulse_stride + (int64_t)i * n2 + t2, val);
+        } else {
+          __stcg(a.dst + pulse * a.pulse_stride + (int64_t)i * n2 + base + b, val);
+        }
+      }
+    }
+  }
+  cp_async_wait_all();
+}
+
+}  // namespace dc
