@@ -34,6 +34,9 @@ struct IonoSmallArgs {
   const float2 *twf, *twi;
   double fs_over_n, fc;
   cudaStream_t stream;
+  const float2 *tw1024;  // 1024-point pass-2 table for the warp-level kernels (n = 1024), or null
+  int grid_cap;          // max CTAs of the persistent grid (0: one wave of the whole GPU)
+  const float2 *gtab;    // per-bin 1/f_k FP32 pairs for the warp-level kernel, or null
 };
 cudaError_t launch_iono_small(const IonoSmallArgs &a, bool distort);
 
@@ -51,7 +54,12 @@ struct FourStepArgs {
   int H;
   double fs_over_n, fc;
   cudaStream_t stream;
+  const float2 *tw1024;       // 1024-point pass-2 table for the warp-level kernels, or null
+  int grid_cap;               // max CTAs of the persistent grid (0: one wave of the whole GPU)
+  const float2 *gtab;         // per-bin 1/f_k FP32 pairs (row layout) for the warp-level row kernel
 };
+// offset (float2 entries) of the NS = 32 section inside the P = 10, radix-32 forward pass table
+int tw1024_offset();
 // pass 0 = A (columns, forward), 1 = B (rows, phase), 2 = C (columns, inverse)
 cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, bool distort);
 
@@ -65,6 +73,7 @@ struct DopplerArgs {
   int64_t pulse_base;
   double carrier_cycles_per_sample;  // fc / fs; carrier phase psi_m = fc (1 - beta) m / fs
   cudaStream_t stream;
+  int grid_cap;  // max CTAs of the persistent grid (0: one wave of the whole GPU)
 };
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
 int doppler_path(double max_abs_beta_m1);

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -41,7 +42,7 @@ dc_status cuda_fail(cudaError_t e, const char *what) {
   } while (0)
 
 constexpr int kRingSlots = 4;
-constexpr int64_t kChunkTargetBytes = 48ll << 20;  // L2-resident working set per chunk (126 MB L2)
+constexpr int64_t kChunkTargetBytes = 512ll << 20;  // pulses per launch group (launch-overhead amortisation)
 
 struct ParamSlot {
   PulseParams *host = nullptr;  // pinned
@@ -67,8 +68,16 @@ struct dc_plan_s {
   // device tables
   float2 *tw_small_f = nullptr, *tw_small_i = nullptr;
   float2 *tw1f = nullptr, *tw1i = nullptr, *tw2f = nullptr, *tw2i = nullptr, *twh = nullptr, *twl = nullptr;
+  const float2 *tw1024 = nullptr;  // radix-32 x 32 pass-2 table inside one of the tables above
+  float2 *gtab = nullptr;          // per-bin 1/f_k as FP32 pairs, in the layout the warp row kernel reads
   float2 *scratch = nullptr;  // chunk * n samples
+  float2 *scratch2 = nullptr;  // second chunk buffer (two chunks in flight on the internal streams)
   int64_t scratch_bytes = 0;
+  // chunk pipelining: consecutive chunks alternate between two internal streams, each kernel
+  // capped at half the SMs, so memory-bound and compute-bound passes of different chunks co-run
+  cudaStream_t ws[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  bool pipeline = false;  // DISPCORR_PIPE=1 enables (measured slower with large chunks; kept for tuning)
   // host-path buffers (lazily allocated)
   float2 *hin[2] = {nullptr, nullptr}, *hout[2] = {nullptr, nullptr};
   int64_t host_chunk = 0;
@@ -94,7 +103,9 @@ namespace {
 
 bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
-// FP32 twiddle tables generated in binary64: section [NS][R], entry r = exp(-2 pi i k r / (NS R)).
+// FP32 twiddle tables generated in binary64.  Pass section of NS*R entries, entry (k, r) =
+// exp(-2 pi i k r / (NS R)) stored at float2 index ((r/2) NS + k) 2 + (r mod 2), i.e. float4 pairs
+// (r even, r odd) ordered [r/2][k] so that lanes with consecutive k read consecutive words.
 std::vector<float2> build_pass_tables(const dc::PlanDesc &d, bool inv) {
   std::vector<float2> t((size_t)std::max(d.tw_size, 2), make_float2(0.f, 0.f));
   for (int i = 0; i < d.npass; ++i) {
@@ -106,7 +117,7 @@ std::vector<float2> build_pass_tables(const dc::PlanDesc &d, bool inv) {
       for (int64_t r = 0; r < R; ++r) {
         const int64_t e = (k * r) % M;
         const double ang = -2.0 * dc::kPi * (double)e / (double)M;
-        t.at((size_t)(off + k * R + r)) = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        t.at((size_t)(off + ((r >> 1) * NS + k) * 2 + (r & 1))) = make_float2((float)std::cos(ang), (float)std::sin(ang));
       }
   }
   return t;
@@ -168,26 +179,33 @@ dc_status stage_params(dc_plan_s *p, int64_t batch, const double *tec, const dou
   p->ring_next = (p->ring_next + 1) % kRingSlots;
   if (s.used) DC_CUDA(cudaEventSynchronize(s.done), "cudaEventSynchronize(param slot)");
   if (s.cap < batch) {
-    if (s.host) cudaFreeHost(s.host);
-    if (s.dev) cudaFree(s.dev);
-    s.host = nullptr;
-    s.dev = nullptr;
-    s.cap = 0;
+    // grow every slot at once so steady-state calls never allocate
     const int64_t cap = std::max<int64_t>(batch, 1024);
-    if (cudaMallocHost(&s.host, sizeof(PulseParams) * cap) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(DC_ERR_OUT_OF_MEMORY, "pinned parameter staging (%lld pulses)", (long long)cap);
+    for (auto &q : p->ring) {
+      if (q.used) DC_CUDA(cudaEventSynchronize(q.done), "cudaEventSynchronize(param slot)");
+      if (q.host) cudaFreeHost(q.host);
+      if (q.dev) cudaFree(q.dev);
+      q.host = nullptr;
+      q.dev = nullptr;
+      q.cap = 0;
+      if (cudaMallocHost(&q.host, sizeof(PulseParams) * cap) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DC_ERR_OUT_OF_MEMORY, "pinned parameter staging (%lld pulses)", (long long)cap);
+      }
+      if (cudaMalloc(&q.dev, sizeof(PulseParams) * cap) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DC_ERR_OUT_OF_MEMORY, "device parameter buffer (%lld pulses)", (long long)cap);
+      }
+      q.cap = cap;
     }
-    if (cudaMalloc(&s.dev, sizeof(PulseParams) * cap) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(DC_ERR_OUT_OF_MEMORY, "device parameter buffer (%lld pulses)", (long long)cap);
-    }
-    s.cap = cap;
   }
   const double k2c = 2.0 * dc::k2_per_tec() / dc::kC;  // nu_k = (2 K2 / c) / f_k, two-way
   double mb = 0.0;
   for (int64_t i = 0; i < batch; ++i) {
     s.host[i].nu_coef = tec ? k2c * tec[i] : 0.0;
+    s.host[i].nu_hi = (float)s.host[i].nu_coef;
+    s.host[i].nu_lo = (float)(s.host[i].nu_coef - (double)s.host[i].nu_hi);
+    s.host[i].pad0 = s.host[i].pad1 = 0.f;
     s.host[i].beta = alpha ? 1.0 / alpha[i] : 1.0;
     mb = std::max(mb, std::fabs(s.host[i].beta - 1.0));
   }
@@ -219,29 +237,37 @@ struct ProfScope {
   dc_plan_s *p;
   int cls;
   int64_t samples;
+  cudaStream_t st;
   cudaEvent_t a = nullptr;
-  ProfScope(dc_plan_s *p_, int cls_, int64_t samples_) : p(p_), cls(cls_), samples(samples_) {
+  ProfScope(dc_plan_s *p_, int cls_, int64_t samples_, cudaStream_t st_)
+      : p(p_), cls(cls_), samples(samples_), st(st_) {
     p->launches += 1;
-    if (p->prof && (a = prof_event(p))) cudaEventRecord(a, p->stream);
+    if (p->prof && (a = prof_event(p))) cudaEventRecord(a, st);
   }
   ~ProfScope() {
     if (a) {
       cudaEvent_t b = prof_event(p);
       if (b) {
-        cudaEventRecord(b, p->stream);
+        cudaEventRecord(b, st);
         p->recs.push_back({cls, samples, a, b});
       }
     }
   }
 };
 
+// where a chunk's kernels go: stream + persistent-grid cap
+struct Lane {
+  cudaStream_t st;
+  int cap;
+};
+
 // ---- stage launchers (no validation) -----------------------------------------------------------
 dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
-                   int64_t pulse_base, bool distort) {
+                   int64_t pulse_base, bool distort, Lane ln) {
   if (p->regime == 0) {
     dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp + pulse_base, p->tw_small_f, p->tw_small_i,
-                        p->fs / (double)p->n, p->fc, p->stream};
-    ProfScope ps(p, DC_K_IONO_SMALL, pulses * p->n);
+                        p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab};
+    ProfScope ps(p, DC_K_IONO_SMALL, pulses * p->n, ln.st);
     DC_CUDA(dc::launch_iono_small(a, distort), "iono_small_kernel launch");
     return DC_OK;
   }
@@ -262,19 +288,63 @@ dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses,
   a.H = p->H;
   a.fs_over_n = p->fs / (double)p->n;
   a.fc = p->fc;
-  a.stream = p->stream;
+  a.stream = ln.st;
+  a.tw1024 = p->tw1024;
+  a.grid_cap = ln.cap;
+  a.gtab = p->gtab;
   for (int pass = 0; pass < 3; ++pass) {
-    ProfScope ps(p, DC_K_FOURSTEP_A + pass, pulses * p->n);
+    ProfScope ps(p, DC_K_FOURSTEP_A + pass, pulses * p->n, ln.st);
     DC_CUDA(dc::launch_iono_fourstep_pass(a, pass, distort), "four-step kernel launch");
   }
   return DC_OK;
 }
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
-                      int64_t pulse_base, double max_abs_beta_m1) {
-  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, p->stream};
-  ProfScope ps(p, DC_K_DOPPLER, pulses * p->n);
+                      int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, ln.cap};
+  ProfScope ps(p, DC_K_DOPPLER, pulses * p->n, ln.st);
   DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
+  return DC_OK;
+}
+
+// internal streams wait for everything enqueued so far on the plan stream; afterwards the plan
+// stream waits for both internal streams (so callers see ordinary stream semantics)
+dc_status fork(dc_plan_s *p) {
+  if (!p->ws[0]) {
+    for (int i = 0; i < 2; ++i) {
+      DC_CUDA(cudaStreamCreateWithFlags(&p->ws[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      DC_CUDA(cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    DC_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  DC_CUDA(cudaEventRecord(p->ev_fork, p->stream), "cudaEventRecord(fork)");
+  for (int i = 0; i < 2; ++i) DC_CUDA(cudaStreamWaitEvent(p->ws[i], p->ev_fork, 0), "cudaStreamWaitEvent(fork)");
+  return DC_OK;
+}
+dc_status join(dc_plan_s *p) {
+  for (int i = 0; i < 2; ++i) {
+    DC_CUDA(cudaEventRecord(p->ev_join[i], p->ws[i]), "cudaEventRecord(join)");
+    DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join[i], 0), "cudaStreamWaitEvent(join)");
+  }
+  return DC_OK;
+}
+
+// chunk buffers for dc_correct: two (for the two internal streams), min(chunk, batch) pulses each
+dc_status ensure_scratch(dc_plan_s *p, int64_t batch) {
+  const int64_t need = std::min(p->chunk, batch) * p->n * (int64_t)sizeof(float2);
+  if (p->scratch_bytes >= need) return DC_OK;
+  DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize(scratch)");
+  for (int i = 0; i < 2; ++i)
+    if (p->ws[i]) DC_CUDA(cudaStreamSynchronize(p->ws[i]), "cudaStreamSynchronize(scratch)");
+  if (p->scratch) cudaFree(p->scratch);
+  if (p->scratch2) cudaFree(p->scratch2);
+  p->scratch = p->scratch2 = nullptr;
+  p->scratch_bytes = 0;
+  if (cudaMalloc(&p->scratch, (size_t)need) != cudaSuccess || cudaMalloc(&p->scratch2, (size_t)need) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DC_ERR_OUT_OF_MEMORY, "chunk buffers (2 x %lld bytes)", (long long)need);
+  }
+  p->scratch_bytes = need;
   return DC_OK;
 }
 
@@ -290,10 +360,15 @@ dc_status iono_common(dc_plan_t p, void *x, int64_t batch, const double *tec, bo
   if ((s = stage_params(p, batch, tec, nullptr, &pp, &slot, nullptr)) != DC_OK) return s;
   float2 *xp = (float2 *)x;
   const int64_t step = (p->regime == 0) ? std::min<int64_t>(batch, 1ll << 30) : p->chunk;
-  for (int64_t b0 = 0; b0 < batch; b0 += step) {
+  const int64_t nchunks = (batch + step - 1) / step;
+  const bool pipe = nchunks > 1 && !p->prof && p->pipeline;
+  if (pipe && (s = fork(p)) != DC_OK) return s;
+  for (int64_t b0 = 0, i = 0; b0 < batch; b0 += step, ++i) {
     const int64_t nb = std::min(step, batch - b0);
-    if ((s = run_iono(p, xp + b0 * p->n, xp + b0 * p->n, nb, pp, b0, distort)) != DC_OK) return s;
+    const Lane ln = pipe ? Lane{p->ws[i & 1], (p->sm_count + 1) / 2} : Lane{p->stream, 0};
+    if ((s = run_iono(p, xp + b0 * p->n, xp + b0 * p->n, nb, pp, b0, distort, ln)) != DC_OK) return s;
   }
+  if (pipe && (s = join(p)) != DC_OK) return s;
   return release_slot(p, slot);
 }
 
@@ -370,6 +445,8 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     dc::describe_small_plan(p->log2n, d);
     if ((s = upload(&p->tw_small_f, build_pass_tables(d, false))) != DC_OK) return cleanup(s);
     if ((s = upload(&p->tw_small_i, build_pass_tables(d, true))) != DC_OK) return cleanup(s);
+    if (p->log2n == 10 && d.npass == 2 && d.log_radix_fwd[0] == 5 && d.log_radix_fwd[1] == 5)
+      p->tw1024 = p->tw_small_f + dc::tw1024_offset();
   } else {
     dc::fourstep_split(p->log2n, p->P1, p->P2);
     dc::PlanDesc d1, d2;
@@ -379,6 +456,9 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     if ((s = upload(&p->tw1i, build_pass_tables(d1, true))) != DC_OK) return cleanup(s);
     if ((s = upload(&p->tw2f, build_pass_tables(d2, false))) != DC_OK) return cleanup(s);
     if ((s = upload(&p->tw2i, build_pass_tables(d2, true))) != DC_OK) return cleanup(s);
+    auto radix32x32 = [](const dc::PlanDesc &d) { return d.npass == 2 && d.log_radix_fwd[0] == 5 && d.log_radix_fwd[1] == 5; };
+    if (p->P2 == 10 && radix32x32(d2)) p->tw1024 = p->tw2f + dc::tw1024_offset();
+    else if (p->P1 == 10 && radix32x32(d1)) p->tw1024 = p->tw1f + dc::tw1024_offset();
     p->H = (p->log2n + 1) / 2;
     std::vector<float2> lo((size_t)1 << p->H), hi((size_t)1 << (p->log2n - p->H));
     for (size_t m = 0; m < lo.size(); ++m) {
@@ -392,13 +472,31 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     if ((s = upload(&p->twl, lo)) != DC_OK) return cleanup(s);
     if ((s = upload(&p->twh, hi)) != DC_OK) return cleanup(s);
   }
-  p->chunk = std::max<int64_t>(1, kChunkTargetBytes / (n * (int64_t)sizeof(float2)));
-  p->chunk = std::min<int64_t>(p->chunk, 65535);
-  p->scratch_bytes = p->chunk * n * (int64_t)sizeof(float2);
-  if (cudaMalloc(&p->scratch, (size_t)p->scratch_bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return cleanup(fail(DC_ERR_OUT_OF_MEMORY, "scratch (%lld bytes)", (long long)p->scratch_bytes));
+  int64_t target = kChunkTargetBytes;
+  if (const char *env = getenv("DISPCORR_CHUNK_MB")) {  // tuning override (benchmarks only)
+    const long v = atol(env);
+    if (v > 0) target = (int64_t)v << 20;
   }
+  p->chunk = std::max<int64_t>(1, target / (n * (int64_t)sizeof(float2)));
+  // per-bin g_k = 1/f_k (0 where f_k <= 0, reading R3) for the warp-level row kernel, FP32 pairs:
+  // regime 0 (n = 1024): natural bin order; four-step with N2 = 1024: row layout [k1][k2] of k = k1 + N1 k2
+  if (p->tw1024) {
+    const int P1 = (p->regime == 0) ? 0 : p->P1;
+    std::vector<float2> g((size_t)n);
+    for (int64_t k1 = 0; k1 < (1ll << P1); ++k1)
+      for (int64_t k2 = 0; k2 < 1024; ++k2) {
+        const int64_t k = k1 + (k2 << P1);
+        const int64_t kk = (k >= n / 2) ? k - n : k;
+        const double f = fc_hz + fs_hz * (double)kk / (double)n;
+        const double gi = (f > 0.0) ? 1.0 / f : 0.0;
+        const float hi = (float)gi;
+        g[(size_t)(k1 * 1024 + k2)] = make_float2(hi, (float)(gi - (double)hi));
+      }
+    if ((s = upload(&p->gtab, g)) != DC_OK) return cleanup(s);
+  }
+  if (const char *env = getenv("DISPCORR_PIPE")) p->pipeline = atoi(env) != 0;
+  p->chunk = std::min<int64_t>(p->chunk, 65535);
+  p->scratch_bytes = 0;  // chunk buffers are allocated on first use, sized to the batch (ensure_scratch)
   for (auto &slot : p->ring)
     if (cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
@@ -410,7 +508,10 @@ dc_status dc_plan_destroy(dc_plan_t p) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->stream);
-  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch,
+  for (int i = 0; i < 2; ++i) {
+    if (p->ws[i]) cudaStreamSynchronize(p->ws[i]);
+  }
+  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab,
                     p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
   for (float2 *b : bufs)
     if (b) cudaFree(b);
@@ -425,6 +526,11 @@ dc_status dc_plan_destroy(dc_plan_t p) {
     if (p->ev_out[i]) cudaEventDestroy(p->ev_out[i]);
   }
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (p->ws[i]) cudaStreamDestroy(p->ws[i]);
+    if (p->ev_join[i]) cudaEventDestroy(p->ev_join[i]);
+  }
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
   if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
   delete p;
@@ -469,7 +575,7 @@ dc_status dc_doppler(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   float2 *yp = (float2 *)y;
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, batch - b0);
-    if ((s = run_doppler(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb)) != DC_OK) return s;
+    if ((s = run_doppler(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
   }
   return release_slot(p, slot);
 }
@@ -484,17 +590,24 @@ dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
   if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
   DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  if ((s = ensure_scratch(p, batch)) != DC_OK) return s;
   PulseParams *pp;
   ParamSlot *slot;
   double mb = 0;
   if ((s = stage_params(p, batch, tec, alpha, &pp, &slot, &mb)) != DC_OK) return s;
   const float2 *xp = (const float2 *)x;
   float2 *yp = (float2 *)y;
-  for (int64_t b0 = 0; b0 < batch; b0 += p->chunk) {
+  const int64_t nchunks = (batch + p->chunk - 1) / p->chunk;
+  const bool pipe = nchunks > 1 && !p->prof && p->pipeline;
+  if (pipe && (s = fork(p)) != DC_OK) return s;
+  for (int64_t b0 = 0, i = 0; b0 < batch; b0 += p->chunk, ++i) {
     const int64_t nb = std::min(p->chunk, batch - b0);
-    if ((s = run_iono(p, xp + b0 * p->n, p->scratch, nb, pp, b0, false)) != DC_OK) return s;
-    if ((s = run_doppler(p, p->scratch, yp + b0 * p->n, nb, pp, b0, mb)) != DC_OK) return s;
+    const Lane ln = pipe ? Lane{p->ws[i & 1], (p->sm_count + 1) / 2} : Lane{p->stream, 0};
+    float2 *scr = (pipe && (i & 1)) ? p->scratch2 : p->scratch;
+    if ((s = run_iono(p, xp + b0 * p->n, scr, nb, pp, b0, false, ln)) != DC_OK) return s;
+    if ((s = run_doppler(p, scr, yp + b0 * p->n, nb, pp, b0, mb, ln)) != DC_OK) return s;
   }
+  if (pipe && (s = join(p)) != DC_OK) return s;
   return release_slot(p, slot);
 }
 
@@ -509,7 +622,12 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
   if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
   DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
-  const int64_t hc = p->chunk;  // pulses per transfer chunk
+  // pulses per transfer chunk: bounded so the pinned-host pipeline overlaps (~64 MiB per copy)
+  const int64_t hc = std::max<int64_t>(1, std::min(p->chunk, (int64_t)(64ll << 20) / (p->n * (int64_t)sizeof(float2))));
+  {
+    dc_status se = ensure_scratch(p, std::min(hc, batch));
+    if (se != DC_OK) return se;
+  }
   if (!p->s_h2d) {
     DC_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking), "cudaStreamCreate");
     DC_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -552,8 +670,8 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
     DC_CUDA(cudaEventRecord(p->ev_in[i], p->s_h2d), "record");
     DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[i], 0), "wait");
     if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[i], 0), "wait");  // hout[i] drained
-    if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, false)) != DC_OK) return s;
-    if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb)) != DC_OK) return s;
+    if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, false, Lane{p->stream, 0})) != DC_OK) return s;
+    if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
     DC_CUDA(cudaEventRecord(p->ev_comp[i], p->stream), "record");
     DC_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[i], 0), "wait");
     DC_CUDA(cudaMemcpyAsync(yh + b0 * pulse_bytes, p->hout[i], nb * pulse_bytes, cudaMemcpyDeviceToHost, p->s_d2h),
@@ -610,7 +728,7 @@ dc_status dc_plan_info(dc_plan_t p, dc_plan_info_t *info) {
   info->n1 = p->regime ? (1ll << p->P1) : 0;
   info->n2 = p->regime ? (1ll << p->P2) : 0;
   info->chunk_pulses = p->chunk;
-  info->scratch_bytes = p->scratch_bytes;
+  info->scratch_bytes = 2 * p->scratch_bytes;
   info->sm_count = p->sm_count;
   info->kernel_launches = p->launches;
   return DC_OK;

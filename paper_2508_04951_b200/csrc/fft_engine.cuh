@@ -79,15 +79,22 @@ __device__ __forceinline__ float2 rot(float2 v) {
     constexpr float sx = (k == 4 || k == 12) ? h : -h;  // sin(2 pi k / 32)
     constexpr float s = INV ? sx : -sx;                   // imaginary part of the rotation
     // (a + ib)(cx + i s) with |cx| = |s| = h: h * ((+-a -+ b) + i(...))
-    float a = v.x, b = v.y;
-    float re = (cx > 0 ? a : -a) - (s > 0 ? b : -b);
-    float im = (s > 0 ? a : -a) + (cx > 0 ? b : -b);
-    return make_float2(re * h, im * h);
+    const float2 p = make_float2(cx > 0 ? v.x : -v.x, s > 0 ? v.x : -v.x);
+    const float2 q = make_float2(s > 0 ? -v.y : v.y, cx > 0 ? v.y : -v.y);
+#if DC_X2
+    return __fmul2_rn(__fadd2_rn(p, q), make_float2(h, h));
+#else
+    return make_float2((p.x + q.x) * h, (p.y + q.y) * h);
+#endif
   } else {
     constexpr float c = cos32(k);
     constexpr float sn = cos32(k - 8);  // sin(2 pi k/32) = cos(2 pi (k-8)/32)
     constexpr float s = INV ? sn : -sn;
+#if DC_X2
+    return __ffma2_rn(make_float2(v.x, v.x), make_float2(c, s), __fmul2_rn(make_float2(v.y, v.y), make_float2(-s, c)));
+#else
     return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
+#endif
   }
 }
 
@@ -250,13 +257,20 @@ struct Tile {
   static constexpr int P = P_;
   static constexpr int L = 1 << P_;
   static constexpr int E = E_;
+  static constexpr int LOGE = (E_ >= 32) ? 5 : (E_ >= 16) ? 4 : (E_ >= 8) ? 3 : (E_ >= 4) ? 2 : 1;
   static constexpr int NB = NB_;
   static constexpr bool ROW = ROW_;
   static constexpr int ELEMS = L * NB;
   static constexpr int T = ELEMS / E;
-  static constexpr int ROWSTRIDE = L + L / 16;  // padded row (ROW tiles): 1 pad slot per 16 samples
-  static constexpr int SMEM_ELEMS = ROW ? NB * ROWSTRIDE : ELEMS;
-  __device__ __forceinline__ static int sidx(int b, int i) { return ROW ? b * ROWSTRIDE + i + (i >> 4) : i * NB + b; }
+  // Bank-conflict padding.  ROW tiles: one pad slot per E samples, so the stride-R stores of
+  // the NS = 1 pass (thread j writes R consecutive samples) land on distinct banks.  COL tiles:
+  // one extra row of NB samples every E rows, so rows R apart alternate 64-byte bank halves.
+  static constexpr int ROWSTRIDE = L + (L >> LOGE);
+  static constexpr int COLROWS = L + (L >> LOGE);
+  static constexpr int SMEM_ELEMS = ROW ? NB * ROWSTRIDE : COLROWS * NB;
+  __device__ __forceinline__ static int sidx(int b, int i) {
+    return ROW ? b * ROWSTRIDE + i + (i >> LOGE) : (i + (i >> LOGE)) * NB + b;
+  }
   // butterfly g of a radix-R pass -> (FFT b, butterfly j)
   template <int R>
   __device__ __forceinline__ static void bmap(int g, int &b, int &j) {
@@ -297,7 +311,7 @@ __device__ __forceinline__ void pass_store_smem(float2 *__restrict__ s, const fl
   }
 }
 
-// twiddle + radix-R DFT.  tw: this pass's table section [NS][R] (entry r = w^(k r)).
+// twiddle + radix-R DFT.  tw: this pass's table section (entry (k, r) = w^(k r), layout [R/2][NS][2]).
 template <class TL, int R, int LOG_NS, bool INV>
 __device__ __forceinline__ void pass_compute(float2 (&v)[TL::E], int tid, const float2 *__restrict__ tw) {
   constexpr int NS = 1 << LOG_NS;
@@ -307,15 +321,15 @@ __device__ __forceinline__ void pass_compute(float2 (&v)[TL::E], int tid, const 
       int b, j;
       TL::template bmap<R>(tid + q * TL::T, b, j);
       int k = j & (NS - 1);
-      const float4 *t4 = reinterpret_cast<const float4 *>(tw + k * R);
+      // table section layout [R/2][NS] of float4 = (w^(k 2h), w^(k (2h+1))): lanes with
+      // consecutive k read consecutive 16-byte words (conflict-free in shared memory)
+      const float4 *t4 = reinterpret_cast<const float4 *>(tw) + k;
       float2 w[R];
-      if constexpr (R >= 2) {
 #pragma unroll
-        for (int h = 0; h < R / 2; ++h) {
-          float4 p = t4[h];  // shared-memory or L1-cached global table
-          w[2 * h] = make_float2(p.x, p.y);
-          w[2 * h + 1] = make_float2(p.z, p.w);
-        }
+      for (int h = 0; h < R / 2; ++h) {
+        float4 p = t4[h * NS];  // shared-memory or L1-cached global table
+        w[2 * h] = make_float2(p.x, p.y);
+        w[2 * h + 1] = make_float2(p.z, p.w);
       }
 #pragma unroll
       for (int r = 1; r < R; ++r) v[q * R + r] = INV ? cmulc(v[q * R + r], w[r]) : cmul(v[q * R + r], w[r]);

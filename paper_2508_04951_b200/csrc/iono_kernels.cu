@@ -12,6 +12,7 @@
 //   plan-owned chunk buffer sized to stay L2-resident, so HBM sees ~16 B / sample.
 #include "dc_kernels.h"
 #include "tile_fft.cuh"
+#include "wfft.cuh"
 
 #include <algorithm>
 
@@ -32,7 +33,7 @@ static constexpr int col_c(int P1) { return (8192 >> P1) < 4 ? 4 : (8192 >> P1);
 static constexpr int row_nb(int P2) { return (8192 >> P2) < 1 ? 1 : (8192 >> P2); }
 
 template <int P, int LOGE, int NB, bool ROW, int MODE, bool DISTORT>
-static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_t st) {
+static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_t st, int cap) {
   using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
   auto kern = tile_fft_kernel<P, LOGE, NB, ROW, MODE, DISTORT>;
   const size_t smem = CFG::smem_bytes(a.H, a.log2n);
@@ -42,17 +43,82 @@ static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CFG::T, smem);
-  const int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
+  int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
   kern<<<(unsigned)grid, CFG::T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
+// ---- warp-level 1024-point kernels (wfft.cuh)
+constexpr bool kRowStage = (DC_ROW_NW == 8);
+static size_t warp_row_smem(int log2n, int H, bool outer) {
+  return RowCfg<DC_ROW_NW, kRowStage>::elems(outer, log2n, H) * sizeof(float2);
+}
+static size_t warp_col_smem(int log2n, int H, bool outer) {
+  size_t e = (size_t)1024 * 8 + (size_t)kWW * (kWPad + 32) + 1024;
+  if (outer) e += (size_t)(1 << H) + (1 << (log2n - H));
+  return e * sizeof(float2);
+}
+template <class K>
+static cudaError_t launch_persistent(K kern, size_t smem, int64_t total, const WarpArgs &a, cudaStream_t st, int cap,
+                                     int nw = kWW) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+  int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  kern<<<(unsigned)grid, nw * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+static cudaError_t launch_warp_row(const WarpArgs &a, bool small, bool distort, cudaStream_t st, int cap) {
+  constexpr int NW = DC_ROW_NW;
+  if (small) {
+    const size_t smem = warp_row_smem(a.log2n, a.H, false);
+    auto k = distort ? warp_row_kernel<MODE_SMALL, true, NW, kRowStage> : warp_row_kernel<MODE_SMALL, false, NW, kRowStage>;
+    return launch_persistent(k, smem, (a.pulses + NW - 1) / NW, a, st, cap, NW);
+  }
+  const int64_t total_w = a.pulses << (a.log2n - 10);
+  const size_t smem = warp_row_smem(a.log2n, a.H, true);
+  auto k = distort ? warp_row_kernel<MODE_ROWB, true, NW, kRowStage> : warp_row_kernel<MODE_ROWB, false, NW, kRowStage>;
+  return launch_persistent(k, smem, (total_w + NW - 1) / NW, a, st, cap, NW);
+}
+static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st, int cap) {
+  const int64_t total = a.pulses * ((1ll << (a.log2n - 10)) / kWW);
+  const size_t smem = warp_col_smem(a.log2n, a.H, !inv);
+  return inv ? launch_persistent(warp_col_kernel<true>, smem, total, a, st, cap)
+             : launch_persistent(warp_col_kernel<false>, smem, total, a, st, cap);
+}
+static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr) {
+  WarpArgs w{};
+  w.src = t.src;
+  w.dst = t.dst;
+  w.pulses = t.pulses;
+  w.pulse_stride = t.pulse_stride;
+  w.pulse_base = t.pulse_base;
+  w.log2n = t.log2n;
+  w.pp = t.pp;
+  w.tw = tw1024;
+  w.twh = t.twh;
+  w.twl = t.twl;
+  w.H = t.H;
+  w.fs_over_n = t.fs_over_n;
+  w.fc = t.fc;
+  w.scale = 1.0f / (float)(1 << t.log2n);
+  w.gtab = gtab;
+  return w;
+}
+// pass-2 section (NS = 32, R = 32) of the P = 10, E = 32 forward table: float4 [r/2][k] layout
+static constexpr int kTw1024Off = PassPlan<10, 5>::tw_off_fwd(1);
+
 template <int P>
-static cudaError_t launch_small_p(const TileArgs &a, bool distort, cudaStream_t st) {
+static cudaError_t launch_small_p(const TileArgs &a, bool distort, cudaStream_t st, int cap) {
   constexpr int NB = small_nb(P);
   const int64_t total = (a.pulses + NB - 1) / NB;
-  return distort ? launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, true>(a, total, st)
-                 : launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, false>(a, total, st);
+  return distort ? launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, true>(a, total, st, cap)
+                 : launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, false>(a, total, st, cap);
 }
 
 cudaError_t launch_iono_small(const IonoSmallArgs &s, bool distort) {
@@ -69,20 +135,21 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, bool distort) {
   a.H = 0;
   a.fs_over_n = s.fs_over_n;
   a.fc = s.fc;
+  if (s.log2n == 10 && s.tw1024 && s.gtab) return launch_warp_row(warp_args(a, s.tw1024, s.gtab), true, distort, s.stream, s.grid_cap);
   switch (s.log2n) {
-    case 1: return launch_small_p<1>(a, distort, s.stream);
-    case 2: return launch_small_p<2>(a, distort, s.stream);
-    case 3: return launch_small_p<3>(a, distort, s.stream);
-    case 4: return launch_small_p<4>(a, distort, s.stream);
-    case 5: return launch_small_p<5>(a, distort, s.stream);
-    case 6: return launch_small_p<6>(a, distort, s.stream);
-    case 7: return launch_small_p<7>(a, distort, s.stream);
-    case 8: return launch_small_p<8>(a, distort, s.stream);
-    case 9: return launch_small_p<9>(a, distort, s.stream);
-    case 10: return launch_small_p<10>(a, distort, s.stream);
-    case 11: return launch_small_p<11>(a, distort, s.stream);
-    case 12: return launch_small_p<12>(a, distort, s.stream);
-    case 13: return launch_small_p<13>(a, distort, s.stream);
+    case 1: return launch_small_p<1>(a, distort, s.stream, s.grid_cap);
+    case 2: return launch_small_p<2>(a, distort, s.stream, s.grid_cap);
+    case 3: return launch_small_p<3>(a, distort, s.stream, s.grid_cap);
+    case 4: return launch_small_p<4>(a, distort, s.stream, s.grid_cap);
+    case 5: return launch_small_p<5>(a, distort, s.stream, s.grid_cap);
+    case 6: return launch_small_p<6>(a, distort, s.stream, s.grid_cap);
+    case 7: return launch_small_p<7>(a, distort, s.stream, s.grid_cap);
+    case 8: return launch_small_p<8>(a, distort, s.stream, s.grid_cap);
+    case 9: return launch_small_p<9>(a, distort, s.stream, s.grid_cap);
+    case 10: return launch_small_p<10>(a, distort, s.stream, s.grid_cap);
+    case 11: return launch_small_p<11>(a, distort, s.stream, s.grid_cap);
+    case 12: return launch_small_p<12>(a, distort, s.stream, s.grid_cap);
+    case 13: return launch_small_p<13>(a, distort, s.stream, s.grid_cap);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -139,48 +206,55 @@ bool describe_fourstep_plan(int P, PlanDesc &d) {
 }
 
 void fourstep_split(int log2n, int &P1, int &P2) {
+  if (log2n >= 17 && log2n <= 21) {  // row pass on the warp-level 1024-point FFT
+    P2 = 10;
+    P1 = log2n - 10;
+    return;
+  }
   P2 = (log2n + 1) / 2;
   if (log2n - P2 > 11) P2 = log2n - 11;
   if (P2 > 13) P2 = 13;
   P1 = log2n - P2;
 }
 
+
+
 template <int P1, int MODE>
-static cudaError_t launch_col_p(const TileArgs &a, cudaStream_t st) {
+static cudaError_t launch_col_p(const TileArgs &a, cudaStream_t st, int cap) {
   constexpr int C = col_c(P1);
   const int64_t total = a.pulses * ((1ll << (a.log2n - P1)) / C);
-  return launch_tile_cfg<P1, DC_FS_LOGE, C, false, MODE, false>(a, total, st);
+  return launch_tile_cfg<P1, DC_FS_LOGE, C, false, MODE, false>(a, total, st, cap);
 }
 
 template <int P2, bool DISTORT>
-static cudaError_t launch_row_p(const TileArgs &a, cudaStream_t st) {
+static cudaError_t launch_row_p(const TileArgs &a, cudaStream_t st, int cap) {
   constexpr int NB = row_nb(P2);
   const int64_t total = a.pulses * ((1ll << (a.log2n - P2)) / NB);
-  return launch_tile_cfg<P2, DC_FS_LOGE, NB, true, MODE_ROWB, DISTORT>(a, total, st);
+  return launch_tile_cfg<P2, DC_FS_LOGE, NB, true, MODE_ROWB, DISTORT>(a, total, st, cap);
 }
 
 template <int MODE>
-static cudaError_t launch_col(int P1, const TileArgs &a, cudaStream_t st) {
+static cudaError_t launch_col(int P1, const TileArgs &a, cudaStream_t st, int cap) {
   switch (P1) {
-    case 7: return launch_col_p<7, MODE>(a, st);
-    case 8: return launch_col_p<8, MODE>(a, st);
-    case 9: return launch_col_p<9, MODE>(a, st);
-    case 10: return launch_col_p<10, MODE>(a, st);
-    case 11: return launch_col_p<11, MODE>(a, st);
+    case 7: return launch_col_p<7, MODE>(a, st, cap);
+    case 8: return launch_col_p<8, MODE>(a, st, cap);
+    case 9: return launch_col_p<9, MODE>(a, st, cap);
+    case 10: return launch_col_p<10, MODE>(a, st, cap);
+    case 11: return launch_col_p<11, MODE>(a, st, cap);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <bool DISTORT>
-static cudaError_t launch_row(int P2, const TileArgs &a, cudaStream_t st) {
+static cudaError_t launch_row(int P2, const TileArgs &a, cudaStream_t st, int cap) {
   switch (P2) {
-    case 7: return launch_row_p<7, DISTORT>(a, st);
-    case 8: return launch_row_p<8, DISTORT>(a, st);
-    case 9: return launch_row_p<9, DISTORT>(a, st);
-    case 10: return launch_row_p<10, DISTORT>(a, st);
-    case 11: return launch_row_p<11, DISTORT>(a, st);
-    case 12: return launch_row_p<12, DISTORT>(a, st);
-    case 13: return launch_row_p<13, DISTORT>(a, st);
+    case 7: return launch_row_p<7, DISTORT>(a, st, cap);
+    case 8: return launch_row_p<8, DISTORT>(a, st, cap);
+    case 9: return launch_row_p<9, DISTORT>(a, st, cap);
+    case 10: return launch_row_p<10, DISTORT>(a, st, cap);
+    case 11: return launch_row_p<11, DISTORT>(a, st, cap);
+    case 12: return launch_row_p<12, DISTORT>(a, st, cap);
+    case 13: return launch_row_p<13, DISTORT>(a, st, cap);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -204,20 +278,27 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, bool dist
       a.src = f.src;
       a.dst = f.dst;
       a.twf = f.tw1f;
-      return launch_col<MODE_COLA>(P1, a, f.stream);
+      if (P1 == 10 && f.tw1024) return launch_warp_col(warp_args(a, f.tw1024), false, f.stream, f.grid_cap);
+      return launch_col<MODE_COLA>(P1, a, f.stream, f.grid_cap);
     case 1:
       a.src = f.dst;
       a.dst = f.dst;
       a.twf = f.tw2f;
       a.twi = f.tw2i;
-      return distort ? launch_row<true>(P2, a, f.stream) : launch_row<false>(P2, a, f.stream);
+      if (P2 == 10 && f.tw1024 && f.gtab) return launch_warp_row(warp_args(a, f.tw1024, f.gtab), false, distort, f.stream, f.grid_cap);
+      return distort ? launch_row<true>(P2, a, f.stream, f.grid_cap) : launch_row<false>(P2, a, f.stream, f.grid_cap);
     case 2:
       a.src = f.dst;
       a.dst = f.dst;
       a.twi = f.tw1i;
-      return launch_col<MODE_COLC>(P1, a, f.stream);
+      if (P1 == 10 && f.tw1024) return launch_warp_col(warp_args(a, f.tw1024), true, f.stream, f.grid_cap);
+      return launch_col<MODE_COLC>(P1, a, f.stream, f.grid_cap);
     default: return cudaErrorInvalidValue;
   }
 }
 
+}  // namespace dc
+
+namespace dc {
+int tw1024_offset() { return kTw1024Off; }
 }  // namespace dc

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
     if constexpr (MODE == MODE_SMALL || MODE == MODE_ROWB) {
       // ---- frequency domain (Eq. 15): registers hold bins k2 = j + r L/RL of FFT b
       constexpr int RL = 1 << PP::log_radix_fwd(NP - 1);
-      const float inv_n = 1.0f / (float)n;
+      const float inv_n = (MODE == MODE_ROWB) ? 1.0f : 1.0f / (float)n;  // ROWB: 1/n applied in pass A
       const int P1 = log2n - P;
 #pragma unroll
       for (int q = 0; q < E / RL; ++q) {
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
         } else if constexpr (MODE == MODE_COLA) {
           const uint32_t t2 = (uint32_t)base + b;
           const uint32_t m = ((uint32_t)i * t2) & nmask;
-          val = cmul(val, cmul(Th[m >> H], Tl[m & hmask]));
+          val = cscale(cmul(val, cmul(Th[m >> H], Tl[m & hmask])), 1.0f / (float)n);  // 1/n (R6) folded here
           __stcg(a.dst + pulse * a.pulse_stride + (int64_t)i * n2 + t2, val);
         } else {
           __stcg(a.dst + pulse * a.pulse_stride + (int64_t)i * n2 + base + b, val);

@@ -1,0 +1,277 @@
+// wfft.cuh -- warp-level 1024-point FFT kernels for the four-step passes of n = 2^17..2^21
+// (and whole 1024-sample pulses).
+//
+// One warp owns one 1024-point FFT: lane j holds the 32 samples x[j + 32 r] in registers,
+// pass 1 is a radix-32 DFT over r (Stockham NS = 1, outputs to j*32 + s), a warp-private
+// padded shared-memory exchange (stride 33: conflict-free) and pass 2 a twiddled radix-32 DFT
+// over the other index; the result X[j + 32 s] is in natural order with the same register
+// ownership that the first inverse pass needs, so forward FFT -> Eq. 15 phase -> inverse FFT
+// never leave the warp.  Warps synchronise only with __syncwarp(), so the 8 warps of a CTA run
+// out of phase and hide each other's shared-memory and FP64 latency (the barrier-lockstep
+// CTA design of tile_fft.cuh left ~2 warps per scheduler stalled in the same phase).
+#pragma once
+#include "tile_fft.cuh"
+
+namespace dc {
+
+constexpr int kWW = 8;  // warps per CTA
+constexpr int kWPad = 1058;  // padded exchange buffer (index i + (i >> 5) < 1056; 2*1058 = 4 mod 16 spreads the CTA store reads)
+
+__device__ __forceinline__ int wpad(int i) { return i + (i >> 5); }
+
+// twiddle of pass 2: w1024^(k r), table layout [r/2][k] float4 (k = lane): conflict-free
+template <bool INV>
+__device__ __forceinline__ void wfft1024(float2 (&v)[32], float2 *__restrict__ wk, const float4 *__restrict__ tw,
+                                         int lane) {
+  DFT<32, INV>::run(v);
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < 32; ++s) wk[wpad(lane * 32 + s)] = v[s];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 32; ++r) v[r] = wk[wpad(lane + 32 * r)];
+#pragma unroll
+  for (int h = 0; h < 16; ++h) {
+    const float4 p = tw[h * 32 + lane];
+    if (h > 0) v[2 * h] = INV ? cmulc(v[2 * h], make_float2(p.x, p.y)) : cmul(v[2 * h], make_float2(p.x, p.y));
+    v[2 * h + 1] = INV ? cmulc(v[2 * h + 1], make_float2(p.z, p.w)) : cmul(v[2 * h + 1], make_float2(p.z, p.w));
+  }
+  DFT<32, INV>::run(v);
+}
+
+// outer-twiddle helper: per-warp table P[s] = w_n^(32 a s mod n), s = 0..31 (one exact
+// two-level lookup per lane), so that w_n^(a (lane + 32 s)) = w_n^(a lane) * P[s].
+__device__ __forceinline__ float2 tw2(uint32_t m, int H, uint32_t hmask, const float2 *Th, const float2 *Tl) {
+  return cmul(Th[m >> H], Tl[m & hmask]);
+}
+
+struct WarpArgs {
+  const float2 *src;
+  float2 *dst;
+  int64_t pulses;
+  int64_t pulse_stride;
+  int64_t pulse_base;
+  int log2n;
+  const PulseParams *pp;
+  const float2 *tw;  // 1024-entry pass-2 table, float4 [r/2][k] layout
+  const float2 *twh, *twl;
+  int H;
+  double fs_over_n, fc;
+  float scale;  // pass A: 1/n (inverse-transform normalisation folded into the outer twiddle)
+  const float2 *gtab;  // per-bin 1/f_k FP32 pairs, row layout [k1][k2] (MODE_SMALL: natural order)
+};
+
+// MODE_ROWB: four-step pass B on rows k1 of Z (N2 = 1024).  MODE_SMALL: whole pulses of 1024.
+// NW warps per CTA.  STAGE: each warp prefetches its next row into a private shared buffer with
+// cp.async (8 warps x 255 registers); !STAGE: rows are loaded straight into registers and the
+// latency is hidden by NW = 16 warps (128 registers each).
+#ifndef DC_ROW_NW
+#define DC_ROW_NW 8
+#endif
+template <int NW, bool STAGE>
+struct RowCfg {
+  static constexpr int STG = STAGE ? 2048 : 0;  // staging per warp (float2): Z row + g row
+  static __host__ __device__ constexpr size_t elems(bool outer, int log2n, int H) {
+    return (size_t)NW * (STG + kWPad + 32) + 1024 + (outer ? ((size_t)(1 << H) + (1 << (log2n - H))) : 0);
+  }
+};
+
+template <int MODE, bool DISTORT, int NW, bool STAGE>
+__global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) {
+  using CFG = RowCfg<NW, STAGE>;
+  extern __shared__ float4 smem4[];
+  float2 *sm = reinterpret_cast<float2 *>(smem4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2 *stg = sm + warp * CFG::STG;                        // per-warp staging (8 KB) if STAGE
+  float2 *wk = sm + NW * CFG::STG + warp * kWPad;            // per-warp exchange
+  float2 *Pw = sm + NW * (CFG::STG + kWPad) + warp * 32;     // per-warp outer-twiddle powers
+  float4 *Tw = reinterpret_cast<float4 *>(sm + NW * (CFG::STG + kWPad + 32));
+  float2 *Th = reinterpret_cast<float2 *>(Tw) + 1024;
+  const int H = a.H;
+  const int log2n = a.log2n;
+  const int n = 1 << log2n;
+  float2 *Tl = Th + (MODE == MODE_ROWB ? (n >> H) : 0);
+  const uint32_t nmask = (uint32_t)n - 1u, hmask = (1u << H) - 1u;
+  const int P1 = log2n - 10;
+  const int64_t rows_per_pulse = (MODE == MODE_ROWB) ? ((int64_t)1 << P1) : 1;
+  const int64_t total = a.pulses * rows_per_pulse;
+  const int64_t gw = (int64_t)blockIdx.x * NW + warp, G = (int64_t)gridDim.x * NW;
+
+  // tables (once per CTA)
+  for (int i = threadIdx.x; i < 512; i += NW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
+  if constexpr (MODE == MODE_ROWB) {
+    for (int i = threadIdx.x; i < (n >> H); i += NW * 32) Th[i] = a.twh[i];
+    for (int i = threadIdx.x; i < (1 << H); i += NW * 32) Tl[i] = a.twl[i];
+  }
+  auto row_ptr = [&](const float2 *base, int64_t it) {
+    const int64_t p = it / rows_per_pulse, k1 = it - p * rows_per_pulse;
+    return base + p * a.pulse_stride + k1 * 1024;
+  };
+  auto stage = [&](int64_t it) {
+    const float4 *g = reinterpret_cast<const float4 *>(row_ptr(a.src, it));
+    const int64_t k1 = it - (it / rows_per_pulse) * rows_per_pulse;
+    const float4 *gt = reinterpret_cast<const float4 *>(a.gtab + k1 * 1024);
+    float4 *s4 = reinterpret_cast<float4 *>(stg);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cp_async16(s4 + lane + 32 * i, g + lane + 32 * i);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cp_async16(s4 + 512 + lane + 32 * i, gt + lane + 32 * i);
+  };
+  int64_t it = gw;
+  if constexpr (STAGE) {
+    if (it < total) stage(it);
+    cp_async_commit_();
+  }
+  __syncthreads();  // tables visible
+
+  for (; it < total; it += G) {
+    float2 v[32];
+    if constexpr (STAGE) {
+      cp_async_wait_all();
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = stg[lane + 32 * r];
+    } else {
+      const float2 *g = row_ptr(a.src, it);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = (MODE == MODE_ROWB) ? __ldcg(g + lane + 32 * r) : __ldcs(g + lane + 32 * r);
+    }
+    const int64_t p = it / rows_per_pulse;
+    const uint32_t k1 = (uint32_t)(it - p * rows_per_pulse);
+
+    wfft1024<false>(v, wk, Tw, lane);
+
+    // ---- Eq. 15 phase of bins k = k1 + N1 k2, k2 = lane + 32 s (MODE_SMALL: k = k2):
+    // nu = nu_coef * g_k with g_k = 1/f_k from the plan table (0 for f_k <= 0, R3), FP32-pair math
+    {
+      const PulseParams pr = a.pp[a.pulse_base + p];
+      const float inv_n = (MODE == MODE_ROWB) ? 1.0f : 1.0f / (float)n;  // ROWB: 1/n applied in pass A
+      const float2 *grow = STAGE ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        const float2 g = grow[lane + 32 * s];
+        const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
+        const float2 w = expm2pi(DISTORT ? -rf : rf);
+        v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
+      }
+      if constexpr (STAGE) {
+        __syncwarp();  // staging (Z row + g row) consumed: prefetch the next row
+        const int64_t nit = it + G;
+        if (nit < total) stage(nit);
+        cp_async_commit_();
+      }
+    }
+
+    wfft1024<true>(v, wk, Tw, lane);
+
+    // ---- outputs t2 = lane + 32 s: conj outer twiddle (ROWB) and coalesced stores
+    float2 *out = const_cast<float2 *>(row_ptr(a.dst, it));
+    if constexpr (MODE == MODE_ROWB) {
+      __syncwarp();
+      Pw[lane] = tw2((32u * k1 * (uint32_t)lane) & nmask, H, hmask, Th, Tl);
+      const float2 base = tw2((k1 * (uint32_t)lane) & nmask, H, hmask, Th, Tl);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 32; ++s) __stcg(out + lane + 32 * s, cmulc(v[s], cmul(base, Pw[s])));
+    } else {
+#pragma unroll
+      for (int s = 0; s < 32; ++s) __stcs(out + lane + 32 * s, v[s]);
+    }
+  }
+  if constexpr (STAGE) cp_async_wait_all();
+}
+
+// Four-step column passes with N1 = 1024: a CTA stages a [1024][8] tile (8 columns t2, 64-byte
+// row segments, coalesced) into padded row-major shared memory (row stride 10 samples); warp w
+// transforms column w entirely in registers (forward + outer twiddle for pass A, inverse for
+// pass C), writes its column into its exchange buffer, and the CTA stores the tile back
+// row-major with 16-byte coalesced stores.
+// staging layout: dense 64-byte rows [1024][8]; the 16-byte chunk c of row r is stored at
+// chunk c ^ ((r >> 1) & 3), so cp.async writes are conflict-free and column reads are 2-way.
+__device__ __forceinline__ int col_sw(int row, int col) {
+  return row * 8 + 2 * ((col >> 1) ^ ((row >> 1) & 3)) + (col & 1);
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a) {
+  extern __shared__ float4 smem4[];
+  float2 *sm = reinterpret_cast<float2 *>(smem4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  float2 *stg = sm;                                    // [1024][8] swizzled staging tile
+  float2 *wkall = sm + 1024 * 8;                       // per-warp exchange buffers
+  float2 *wk = wkall + warp * kWPad;
+  float2 *Pw = wkall + kWW * kWPad + warp * 32;
+  float4 *Tw = reinterpret_cast<float4 *>(wkall + kWW * (kWPad + 32));
+  float2 *Th = reinterpret_cast<float2 *>(Tw) + 1024;
+  const int H = a.H;
+  const int log2n = a.log2n;
+  const int n = 1 << log2n;
+  float2 *Tl = Th + (!INV ? (n >> H) : 0);
+  const uint32_t nmask = (uint32_t)n - 1u, hmask = (1u << H) - 1u;
+  const int n2 = n >> 10;
+  const int64_t tiles_per_pulse = n2 / kWW;
+  const int64_t total = a.pulses * tiles_per_pulse;
+
+  for (int i = tid; i < 512; i += kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
+  if constexpr (!INV) {
+    for (int i = tid; i < (n >> H); i += kWW * 32) Th[i] = a.twh[i];
+    for (int i = tid; i < (1 << H); i += kWW * 32) Tl[i] = a.twl[i];
+  }
+  auto stage = [&](int64_t it) {
+    const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
+    const float2 *g = a.src + p * a.pulse_stride + c0;
+#pragma unroll 4
+    for (int i = tid; i < 1024 * 4; i += kWW * 32) {
+      const int row = i >> 2, v4 = i & 3;
+      cp_async16(stg + col_sw(row, 2 * v4), g + (int64_t)row * n2 + 2 * v4);
+    }
+  };
+  int64_t it = blockIdx.x;
+  if (it < total) stage(it);
+  cp_async_commit_();
+
+  for (; it < total; it += gridDim.x) {
+    cp_async_wait_all();
+    __syncthreads();  // tile staged (and, on the first pass, tables visible)
+    float2 v[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = stg[col_sw(lane + 32 * r, warp)];
+    __syncthreads();  // staging tile free
+    const int64_t nit = it + gridDim.x;
+    if (nit < total) stage(nit);
+    cp_async_commit_();
+    const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
+
+    if constexpr (!INV) {
+      wfft1024<false>(v, wk, Tw, lane);
+      // outputs k1 = lane + 32 s of column t2: times w_n^(k1 t2)
+      const uint32_t t2 = (uint32_t)(c0 + warp);
+      __syncwarp();
+      Pw[lane] = tw2((32u * t2 * (uint32_t)lane) & nmask, H, hmask, Th, Tl);
+      // the 1/n of the inverse transform (R6) is folded into pass A's twiddle
+      const float2 base = cscale(tw2((t2 * (uint32_t)lane) & nmask, H, hmask, Th, Tl), a.scale);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 32; ++s) v[s] = cmul(v[s], cmul(base, Pw[s]));
+    } else {
+      wfft1024<true>(v, wk, Tw, lane);
+    }
+    // column (in natural row order lane + 32 s) -> own exchange buffer, then cooperative store
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 32; ++s) wk[wpad(lane + 32 * s)] = v[s];
+    __syncthreads();
+    float2 *g = a.dst + p * a.pulse_stride + c0;
+#pragma unroll 4
+    for (int i = tid; i < 1024 * 4; i += kWW * 32) {
+      const int row = i >> 2, v4 = i & 3;
+      const float2 e0 = wkall[(2 * v4) * kWPad + wpad(row)];
+      const float2 e1 = wkall[(2 * v4 + 1) * kWPad + wpad(row)];
+      __stcg(reinterpret_cast<float4 *>(g + (int64_t)row * n2 + 2 * v4), make_float4(e0.x, e0.y, e1.x, e1.y));
+    }
+    // next iteration's first __syncthreads orders these reads before the exchange buffers are reused
+  }
+  cp_async_wait_all();
+}
+
+}  // namespace dc
