@@ -31,6 +31,8 @@
 #include <type_traits>
 
 #include "dc_kernels.h"
+#include "tma.cuh"
+#include "tma_host.h"
 
 namespace dc {
 
@@ -70,20 +72,23 @@ __device__ __forceinline__ DopTile dop_tile(int64_t item, int64_t tiles_per_puls
   const double halfW = 0.5 * (double)W;
   const int lo_shift = (t.beta < 1.0) ? 1 : 0;
   t.Bcta = (int64_t)floor((double)t.m0 * t.beta - halfW) + 1 - lo_shift;
+  t.Bcta -= (t.Bcta & 1);  // TMA boxes must start 16-byte aligned: even sample index
   const int64_t mlast = t.m0 + kDopM - 1;
   const int64_t Kend = (int64_t)floor((double)mlast * t.beta - halfW) + 1 + W + kDopR + 4;
   t.span = (int)(Kend - t.Bcta);
   return t;
 }
 
-// stage x[Bcta, Bcta + span) of the tile's pulse into shared memory (zeros outside [0, n))
-__device__ __forceinline__ void dop_stage(float2 *buf, const DopTile &t, const float2 *__restrict__ x, int64_t n) {
-  const float2 *xp = x + t.pulse * n;
-  for (int i = threadIdx.x; i < t.span; i += kDopT) {
-    const int64_t k = t.Bcta + i;
-    const bool ok = (k >= 0 && k < n);
-    cp_async8(buf + i, xp + (ok ? k : 0), ok);
-  }
+// stage x[Bcta, Bcta + span) of the tile's pulse into shared memory with the TMA engine:
+// ceil(span / 256) boxes of 256 samples; coordinates outside [0, n) are zero-filled by hardware
+// (R12).  Issued by one thread; completion is the buffer's transaction-count mbarrier.
+constexpr int kDopBox = 256;
+__device__ __forceinline__ int dop_nbox(const DopTile &t) { return (t.span + kDopBox - 1) / kDopBox; }
+__device__ __forceinline__ void dop_stage_tma(float2 *buf, const DopTile &t, const CUtensorMap *xmap, uint64_t *bar) {
+  const int nb = dop_nbox(t);
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, (unsigned)(nb * kDopBox * sizeof(float2)));
+  for (int i = 0; i < nb; ++i) tma_load_2d(buf + i * kDopBox, xmap, (int)(t.Bcta + i * kDopBox), (int)t.pulse, bar);
 }
 
 // sinc weight w = sinc(d), w1 = sinc'(d), w2 = sinc''(d) at d = u - m (u in [-1/2, 1/2]):
@@ -103,12 +108,13 @@ __device__ __forceinline__ void tap_w(float u, int m, float S, float Cc, float &
 // WT > 0: the tap count W is a compile-time constant (fully unrolled tap loop); WT = 0: runtime W.
 template <bool SECOND, int WT>
 __global__ void __launch_bounds__(kDopT, 2)
-    doppler_pipe_kernel(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t n, int W_rt,
+    doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
                         int buf_elems) {
-  extern __shared__ float4 xs4[];
+  extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);
   float2 *ob = xs + 2 * buf_elems;  // output staging for coalesced stores
+  uint64_t *bars = reinterpret_cast<uint64_t *>(ob + kDopM);  // one mbarrier per staging buffer
   const int W = (WT > 0) ? WT : W_rt;
   const int tid = threadIdx.x;
   const int64_t tiles_per_pulse = (n + kDopM - 1) / kDopM;
@@ -116,21 +122,26 @@ __global__ void __launch_bounds__(kDopT, 2)
   const double halfW = 0.5 * (double)W;
   int64_t item = blockIdx.x;
   if (item >= total) return;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   DopTile cur = dop_tile(item, tiles_per_pulse, W, pp, pulse_base);
-  dop_stage(xs, cur, x, n);
-  cp_async_commit();
+  if (tid == 0) dop_stage_tma(xs, cur, &xmap, &bars[0]);
   int bsel = 0;
+  unsigned phase[2] = {0u, 0u};
   for (; item < total; item += gridDim.x) {
-    // ---- prefetch the next tile into the other buffer
+    // ---- prefetch the next tile into the other buffer (its readers finished at the last barrier)
     const int64_t nitem = item + gridDim.x;
     DopTile nxt;
     if (nitem < total) {
       nxt = dop_tile(nitem, tiles_per_pulse, W, pp, pulse_base);
-      dop_stage(xs + (bsel ^ 1) * buf_elems, nxt, x, n);
+      if (tid == 0) dop_stage_tma(xs + (bsel ^ 1) * buf_elems, nxt, &xmap, &bars[bsel ^ 1]);
     }
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
+    mbar_wait(&bars[bsel], phase[bsel]);
+    phase[bsel] ^= 1u;
     const float2 *sb = xs + bsel * buf_elems;
 
     // ---- this thread's R consecutive outputs: exact binary64 window bookkeeping
@@ -287,10 +298,10 @@ __global__ void __launch_bounds__(kDopT, 2)
         for (int i = tid; i < valid; i += kDopT) yp[i] = ob[i];
       }
     }
+    __syncthreads();  // output staging and input buffer bsel free for reuse
     cur = nxt;
     bsel ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 // Exact-tap, one-output-per-thread path (Alg. 1 structure) for any alpha.
@@ -341,8 +352,15 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   const int64_t tiles = (a.n + kDopM - 1) / kDopM * a.pulses;
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
   const int span = (int)(kDopM * (1.0 + kDopMaxDrift)) + a.taps + kDopR + 16;
-  const int buf = (span + 1) & ~1;
-  const size_t smem = sizeof(float2) * (2 * (size_t)buf + kDopM);
+  const int buf = (span + kDopBox - 1) / kDopBox * kDopBox;  // whole TMA boxes
+  const size_t smem = sizeof(float2) * (2 * (size_t)buf + kDopM) + 2 * sizeof(uint64_t) + 1024;
+  CUtensorMap xmap;
+  {
+    const uint64_t dims[2] = {(uint64_t)a.n, (uint64_t)a.pulses};
+    const uint64_t strides[1] = {(uint64_t)a.n * sizeof(float2)};
+    const uint32_t box[2] = {(uint32_t)kDopBox, 1u};
+    if (!encode_tile_map(&xmap, a.x, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  }
   auto kern = doppler_pipe_kernel<SECOND, WT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -352,7 +370,7 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDopT, smem);
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
-  kern<<<(unsigned)grid, kDopT, smem, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample,
+  kern<<<(unsigned)grid, kDopT, smem, a.stream>>>(xmap, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample,
                                                   a.pulses, buf);
   return cudaGetLastError();
 }

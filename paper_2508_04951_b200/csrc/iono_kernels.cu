@@ -13,6 +13,7 @@
 #include "dc_kernels.h"
 #include "tile_fft.cuh"
 #include "wfft.cuh"
+#include "tma_host.h"
 
 #include <algorithm>
 
@@ -55,9 +56,9 @@ static size_t warp_row_smem(int log2n, int H, bool outer) {
   return RowCfg<DC_ROW_NW, kRowStage>::elems(outer, log2n, H) * sizeof(float2);
 }
 static size_t warp_col_smem(int log2n, int H, bool outer) {
-  size_t e = (size_t)1024 * 8 + (size_t)kWW * (kWPad + 32) + 1024;
+  size_t e = (size_t)2 * 1024 * 8 + (size_t)kWW * (kWPad + 32) + 1024;
   if (outer) e += (size_t)(1 << H) + (1 << (log2n - H));
-  return e * sizeof(float2);
+  return e * sizeof(float2) + 2 * sizeof(uint64_t) + 1024;  // + mbarriers, alignment slack
 }
 template <class K>
 static cudaError_t launch_persistent(K kern, size_t smem, int64_t total, const WarpArgs &a, cudaStream_t st, int cap,
@@ -88,8 +89,24 @@ static cudaError_t launch_warp_row(const WarpArgs &a, bool small, bool distort, 
 static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st, int cap) {
   const int64_t total = a.pulses * ((1ll << (a.log2n - 10)) / kWW);
   const size_t smem = warp_col_smem(a.log2n, a.H, !inv);
-  return inv ? launch_persistent(warp_col_kernel<true>, smem, total, a, st, cap)
-             : launch_persistent(warp_col_kernel<false>, smem, total, a, st, cap);
+  // source tensor {t2, t1, pulse} of 8-byte samples, box {8 columns, 256 rows, 1}, 64-byte swizzle
+  CUtensorMap smap;
+  const int n2 = 1 << (a.log2n - 10);
+  const uint64_t dims[3] = {(uint64_t)n2, 1024, (uint64_t)a.pulses};
+  const uint64_t strides[2] = {(uint64_t)n2 * sizeof(float2), (uint64_t)a.pulse_stride * sizeof(float2)};
+  const uint32_t box[3] = {(uint32_t)kWW, 256, 1};
+  if (!encode_tile_map(&smap, a.src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+  auto kern = inv ? warp_col_kernel<true> : warp_col_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWW * 32, smem);
+  int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  kern<<<(unsigned)grid, kWW * 32, smem, st>>>(a, smap);
+  return cudaGetLastError();
 }
 static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr) {
   WarpArgs w{};

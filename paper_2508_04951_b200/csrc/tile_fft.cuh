@@ -27,6 +27,7 @@ __device__ __forceinline__ void cp_async16_zfill(void *smem_dst, const void *gsr
 }
 __device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 enum TileMode { MODE_SMALL = 0, MODE_COLA = 1, MODE_ROWB = 2, MODE_COLC = 3 };
 

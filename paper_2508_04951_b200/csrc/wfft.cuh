@@ -11,6 +11,7 @@
 // CTA design of tile_fft.cuh left ~2 warps per scheduler stalled in the same phase).
 #pragma once
 #include "tile_fft.cuh"
+#include "tma.cuh"
 
 namespace dc {
 
@@ -107,19 +108,25 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
     const int64_t p = it / rows_per_pulse, k1 = it - p * rows_per_pulse;
     return base + p * a.pulse_stride + k1 * 1024;
   };
-  auto stage = [&](int64_t it) {
+  // two cp.async groups per row: the Z row (needed first) and the g row (needed at the phase)
+  auto stage_z = [&](int64_t it) {
     const float4 *g = reinterpret_cast<const float4 *>(row_ptr(a.src, it));
-    const int64_t k1 = it - (it / rows_per_pulse) * rows_per_pulse;
-    const float4 *gt = reinterpret_cast<const float4 *>(a.gtab + k1 * 1024);
     float4 *s4 = reinterpret_cast<float4 *>(stg);
 #pragma unroll
     for (int i = 0; i < 16; ++i) cp_async16(s4 + lane + 32 * i, g + lane + 32 * i);
+  };
+  auto stage_g = [&](int64_t it) {
+    const int64_t k1 = it - (it / rows_per_pulse) * rows_per_pulse;
+    const float4 *gt = reinterpret_cast<const float4 *>(a.gtab + k1 * 1024);
+    float4 *s4 = reinterpret_cast<float4 *>(stg);
 #pragma unroll
     for (int i = 0; i < 16; ++i) cp_async16(s4 + 512 + lane + 32 * i, gt + lane + 32 * i);
   };
   int64_t it = gw;
   if constexpr (STAGE) {
-    if (it < total) stage(it);
+    if (it < total) stage_z(it);
+    cp_async_commit_();
+    if (it < total) stage_g(it);
     cp_async_commit_();
   }
   __syncthreads();  // tables visible
@@ -127,10 +134,13 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
   for (; it < total; it += G) {
     float2 v[32];
     if constexpr (STAGE) {
-      cp_async_wait_all();
+      cp_async_wait_1();  // Z row of this item landed (its g row may still be in flight)
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = stg[lane + 32 * r];
+      __syncwarp();  // Z staging consumed: prefetch the next Z row now
+      if (it + G < total) stage_z(it + G);
+      cp_async_commit_();
     } else {
       const float2 *g = row_ptr(a.src, it);
 #pragma unroll
@@ -146,6 +156,10 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
     {
       const PulseParams pr = a.pp[a.pulse_base + p];
       const float inv_n = (MODE == MODE_ROWB) ? 1.0f : 1.0f / (float)n;  // ROWB: 1/n applied in pass A
+      if constexpr (STAGE) {
+        cp_async_wait_1();  // this item's g row landed (the next Z row may still be in flight)
+        __syncwarp();
+      }
       const float2 *grow = STAGE ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
 #pragma unroll
       for (int s = 0; s < 32; ++s) {
@@ -155,9 +169,8 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
         v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
       }
       if constexpr (STAGE) {
-        __syncwarp();  // staging (Z row + g row) consumed: prefetch the next row
-        const int64_t nit = it + G;
-        if (nit < total) stage(nit);
+        __syncwarp();  // g staging consumed: prefetch the next g row
+        if (it + G < total) stage_g(it + G);
         cp_async_commit_();
       }
     }
@@ -192,13 +205,17 @@ __device__ __forceinline__ int col_sw(int row, int col) {
   return row * 8 + 2 * ((col >> 1) ^ ((row >> 1) & 3)) + (col & 1);
 }
 
+// Staging: the TMA engine loads the [1024][8] tile as four 256-row boxes of a 3-D tensor map
+// {t2 (n2), t1 (1024), pulse} with SWIZZLE_64B, which is exactly the col_sw() layout (16-byte
+// chunk index XOR address bits 7-8), so column reads are 2-way and no LSU instructions are spent
+// on staging.  Two staging buffers (2 tiles in flight), one transaction mbarrier each.
 template <bool INV>
-__global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a) {
-  extern __shared__ float4 smem4[];
+__global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
+  extern __shared__ __align__(1024) float4 smem4[];
   float2 *sm = reinterpret_cast<float2 *>(smem4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  float2 *stg = sm;                                    // [1024][8] swizzled staging tile
-  float2 *wkall = sm + 1024 * 8;                       // per-warp exchange buffers
+  float2 *stg0 = sm;                                   // 2 x [1024][8] swizzled staging tiles
+  float2 *wkall = sm + 2 * 1024 * 8;                   // per-warp exchange buffers
   float2 *wk = wkall + warp * kWPad;
   float2 *Pw = wkall + kWW * kWPad + warp * 32;
   float4 *Tw = reinterpret_cast<float4 *>(wkall + kWW * (kWPad + 32));
@@ -217,29 +234,37 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a)
     for (int i = tid; i < (n >> H); i += kWW * 32) Th[i] = a.twh[i];
     for (int i = tid; i < (1 << H); i += kWW * 32) Tl[i] = a.twl[i];
   }
-  auto stage = [&](int64_t it) {
+  uint64_t *bars = reinterpret_cast<uint64_t *>(Tl + (!INV ? (1 << H) : 0));
+  auto stage = [&](int64_t it, float2 *stg, uint64_t *bar) {  // thread 0 only
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
-    const float2 *g = a.src + p * a.pulse_stride + c0;
-#pragma unroll 4
-    for (int i = tid; i < 1024 * 4; i += kWW * 32) {
-      const int row = i >> 2, v4 = i & 3;
-      cp_async16(stg + col_sw(row, 2 * v4), g + (int64_t)row * n2 + 2 * v4);
-    }
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, 1024 * 8 * sizeof(float2));
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tma_load_3d(stg + b * 256 * 8, &smap, (int)c0, b * 256, (int)p, bar);
   };
+  // two tiles in flight: tile i computes while tiles i+1 and i+2 stream in
   int64_t it = blockIdx.x;
-  if (it < total) stage(it);
-  cp_async_commit_();
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+    if (it < total) stage(it, stg0, &bars[0]);
+    if (it + gridDim.x < total) stage(it + gridDim.x, stg0 + 8192, &bars[1]);
+  }
+  __syncthreads();  // tables and barrier initialisation visible
+  int bsel = 0;
+  unsigned phase[2] = {0u, 0u};
 
-  for (; it < total; it += gridDim.x) {
-    cp_async_wait_all();
-    __syncthreads();  // tile staged (and, on the first pass, tables visible)
+  for (; it < total; it += gridDim.x, bsel ^= 1) {
+    float2 *stg = stg0 + bsel * 8192;
+    mbar_wait(&bars[bsel], phase[bsel]);
+    phase[bsel] ^= 1u;
     float2 v[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) v[r] = stg[col_sw(lane + 32 * r, warp)];
     __syncthreads();  // staging tile free
-    const int64_t nit = it + gridDim.x;
-    if (nit < total) stage(nit);
-    cp_async_commit_();
+    const int64_t nit = it + 2 * (int64_t)gridDim.x;
+    if (tid == 0 && nit < total) stage(nit, stg, &bars[bsel]);
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
 
     if constexpr (!INV) {
@@ -269,9 +294,8 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a)
       const float2 e1 = wkall[(2 * v4 + 1) * kWPad + wpad(row)];
       __stcg(reinterpret_cast<float4 *>(g + (int64_t)row * n2 + 2 * v4), make_float4(e0.x, e0.y, e1.x, e1.y));
     }
-    // next iteration's first __syncthreads orders these reads before the exchange buffers are reused
+    __syncthreads();  // exchange buffers free before the next tile's FFT reuses them
   }
-  cp_async_wait_all();
 }
 
 }  // namespace dc
