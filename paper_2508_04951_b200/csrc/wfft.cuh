@@ -45,6 +45,14 @@ __device__ __forceinline__ void wfft1024(float2 (&v)[32], float2 *__restrict__ w
 __device__ __forceinline__ float2 tw2(uint32_t m, int H, uint32_t hmask, const float2 *Th, const float2 *Tl) {
   return cmul(Th[m >> H], Tl[m & hmask]);
 }
+// w_n^m = exp(-2 pi i m / n) for 0 <= m < n = 2^log2n via sincospif of the exact FP32 argument
+// 2 m / n (m < 2^24 is exact in FP32): ~1 ulp, no table, no shared-memory bank conflicts.
+__device__ __forceinline__ float2 twn(uint32_t m, int log2n) {
+  const float x = __uint2float_rn(m) * __int_as_float((127 + 1 - log2n) << 23);  // 2 m / n
+  float sn, cs;
+  sincospif(x, &sn, &cs);
+  return make_float2(cs, -sn);
+}
 
 struct WarpArgs {
   const float2 *src;
@@ -100,10 +108,9 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
 
   // tables (once per CTA)
   for (int i = threadIdx.x; i < 512; i += NW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  if constexpr (MODE == MODE_ROWB) {
-    for (int i = threadIdx.x; i < (n >> H); i += NW * 32) Th[i] = a.twh[i];
-    for (int i = threadIdx.x; i < (1 << H); i += NW * 32) Tl[i] = a.twl[i];
-  }
+  (void)Th;
+  (void)Tl;
+  (void)hmask;  // outer twiddles come from twn() (sincospif), not the two-level table
   auto row_ptr = [&](const float2 *base, int64_t it) {
     const int64_t p = it / rows_per_pulse, k1 = it - p * rows_per_pulse;
     return base + p * a.pulse_stride + k1 * 1024;
@@ -181,8 +188,8 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
     float2 *out = const_cast<float2 *>(row_ptr(a.dst, it));
     if constexpr (MODE == MODE_ROWB) {
       __syncwarp();
-      Pw[lane] = tw2((32u * k1 * (uint32_t)lane) & nmask, H, hmask, Th, Tl);
-      const float2 base = tw2((k1 * (uint32_t)lane) & nmask, H, hmask, Th, Tl);
+      Pw[lane] = twn((32u * k1 * (uint32_t)lane) & nmask, log2n);
+      const float2 base = twn((k1 * (uint32_t)lane) & nmask, log2n);
       __syncwarp();
 #pragma unroll
       for (int s = 0; s < 32; ++s) __stcg(out + lane + 32 * s, cmulc(v[s], cmul(base, Pw[s])));
@@ -230,10 +237,7 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a,
   const int64_t total = a.pulses * tiles_per_pulse;
 
   for (int i = tid; i < 512; i += kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  if constexpr (!INV) {
-    for (int i = tid; i < (n >> H); i += kWW * 32) Th[i] = a.twh[i];
-    for (int i = tid; i < (1 << H); i += kWW * 32) Tl[i] = a.twl[i];
-  }
+  (void)hmask;  // outer twiddles come from twn() (sincospif), not the two-level table
   uint64_t *bars = reinterpret_cast<uint64_t *>(Tl + (!INV ? (1 << H) : 0));
   auto stage = [&](int64_t it, float2 *stg, uint64_t *bar) {  // thread 0 only
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
@@ -272,9 +276,9 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a,
       // outputs k1 = lane + 32 s of column t2: times w_n^(k1 t2)
       const uint32_t t2 = (uint32_t)(c0 + warp);
       __syncwarp();
-      Pw[lane] = tw2((32u * t2 * (uint32_t)lane) & nmask, H, hmask, Th, Tl);
+      Pw[lane] = twn((32u * t2 * (uint32_t)lane) & nmask, log2n);
       // the 1/n of the inverse transform (R6) is folded into pass A's twiddle
-      const float2 base = cscale(tw2((t2 * (uint32_t)lane) & nmask, H, hmask, Th, Tl), a.scale);
+      const float2 base = cscale(twn((t2 * (uint32_t)lane) & nmask, log2n), a.scale);
       __syncwarp();
 #pragma unroll
       for (int s = 0; s < 32; ++s) v[s] = cmul(v[s], cmul(base, Pw[s]));
