@@ -271,9 +271,21 @@ def main():
         g = 16.0 * fft_samples / (fft_ms / 1e3) / 1e9
         fft_stage = {"kernels": fft_names, "gbs": g, "frac_hbm": g / hbm,
                      "samples_per_s": fft_samples / (fft_ms / 1e3)}
+    # measured DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (profiles/r1_traffic.json: DRAM bytes per sample), scaled to this launch size
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    kname = {"fourstep_A": "warp_col_kernel<0>", "fourstep_B": "warp_row_kernel<2", "fourstep_C": "warp_col_kernel<1>",
+             "doppler": "doppler_pipe_kernel<0, 32>"}.get(dom)
+    if os.path.exists(tfile) and kname and n == (1 << 20):
+        per = json.load(open(tfile))["dram_bytes_per_sample"]
+        hit = [v for k, v in per.items() if kname in k]
+        if hit:
+            traffic = hit[0] * kern[dom]["samples_per_launch"]
     roofline = {"bound": "hbm", "achieved": kern[dom]["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": kern[dom]["gbs"] / hbm, "traffic": None, "kernel": dom, "peak_source": peak_kind,
-                "bytes_per_sample": 16, "kernels": kern, "fft_stage": fft_stage}
+                "frac": kern[dom]["gbs"] / hbm, "traffic": traffic, "kernel": dom, "peak_source": peak_kind,
+                "bytes_per_sample": 16, "algorithmic_bytes_per_launch": 16 * kern[dom]["samples_per_launch"],
+                "kernels": kern, "fft_stage": fft_stage}
 
     # ---------------- end to end through the public host-buffer API (pinned host memory)
     e2e = None
