@@ -244,39 +244,59 @@ def main():
     clocks = clk.summary()
 
     # ---------------- per-kernel timing pass (CUDA events around each launch, plan stream)
-    plan.profile_enable(True)
-    for _ in range(args.steps):
-        step()
-    prof = plan.profile_read()
-    plan.profile_enable(False)
     hbm, sm_max, peak_kind = peaks()
-    kern = {}
-    for name, d in prof.items():
-        if d["launches"] == 0:
-            continue
-        sec = d["ms"] / 1e3
-        gbs = 16.0 * d["samples"] / sec / 1e9  # algorithmic: read 8 B + write 8 B per sample
-        kern[name] = {"launches": d["launches"], "ms_per_launch": d["ms"] / d["launches"],
-                      "samples_per_launch": d["samples"] // d["launches"], "gbs": gbs, "frac_hbm": gbs / hbm}
-        if name == "doppler":
-            tfl = 4.0 * taps * d["samples"] / sec / 1e12
-            kern[name]["tflops"] = tfl
-            kern[name]["frac_fp32"] = tfl / (148 * 128 * 2 * sm_max * 1e6 / 1e12)
+
+    def profile(pl):
+        pl.profile_enable(True)
+        for _ in range(args.steps):
+            pl.correct(x, y, tec_r, alpha_r)
+        pr = pl.profile_read()
+        pl.profile_enable(False)
+        out = {}
+        for name, d in pr.items():
+            if d["launches"] == 0:
+                continue
+            sec = d["ms"] / 1e3
+            gbs = 16.0 * d["samples"] / sec / 1e9  # algorithmic: read 8 B + write 8 B per sample
+            out[name] = {"launches": d["launches"], "ms_per_launch": d["ms"] / d["launches"],
+                         "samples_per_launch": d["samples"] // d["launches"], "gbs": gbs, "frac_hbm": gbs / hbm}
+            if name in ("doppler", "fused"):
+                tfl = 4.0 * taps * d["samples"] / sec / 1e12
+                out[name]["tflops_sinc"] = tfl
+                out[name]["frac_fp32"] = tfl / (148 * 128 * 2 * sm_max * 1e6 / 1e12)
+        return out
+
+    kern = profile(plan)
+    # per-stage breakdown with the multi-kernel schedule (same kernels' arithmetic, one launch per
+    # stage per launch group): a separate plan built with DISPCORR_FUSED=0
+    stages = None
+    if "fused" in kern:
+        old = os.environ.get("DISPCORR_FUSED")
+        os.environ["DISPCORR_FUSED"] = "0"
+        plan_s = dc.Plan(n, FS, 0.0, taps=taps, stream=stream)
+        if old is None:
+            del os.environ["DISPCORR_FUSED"]
+        else:
+            os.environ["DISPCORR_FUSED"] = old
+        plan_s.correct(x, y, tec_r, alpha_r)
+        stages = profile(plan_s)
+        plan_s.close()
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches"])
-    fft_names = [k for k in kern if k != "doppler"]
-    fft_ms = sum(prof[k]["ms"] for k in fft_names)
-    fft_samples = prof[fft_names[0]]["samples"] if fft_names else 0
+    src = stages if stages else kern
+    fft_names = [k for k in src if k not in ("doppler", "fused")]
     fft_stage = None
-    if fft_ms > 0:
+    if fft_names:
+        fft_ms = sum(src[k]["ms_per_launch"] * src[k]["launches"] for k in fft_names)
+        fft_samples = src[fft_names[0]]["samples_per_launch"] * src[fft_names[0]]["launches"]
         g = 16.0 * fft_samples / (fft_ms / 1e3) / 1e9
-        fft_stage = {"kernels": fft_names, "gbs": g, "frac_hbm": g / hbm,
-                     "samples_per_s": fft_samples / (fft_ms / 1e3)}
+        fft_stage = {"kernels": fft_names, "schedule": "multi-kernel" if stages else "as run", "gbs": g,
+                     "frac_hbm": g / hbm, "samples_per_s": fft_samples / (fft_ms / 1e3)}
     # measured DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (profiles/r1_traffic.json: DRAM bytes per sample), scaled to this launch size
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "r1_traffic.json")
     kname = {"fourstep_A": "warp_col_kernel<0>", "fourstep_B": "warp_row_kernel<2", "fourstep_C": "warp_col_kernel<1>",
-             "doppler": "doppler_pipe_kernel<0, 32>"}.get(dom)
+             "doppler": "doppler_pipe_kernel<0, 32>", "fused": "fused_correct_kernel<0, 32>"}.get(dom)
     if os.path.exists(tfile) and kname and n == (1 << 20):
         per = json.load(open(tfile))["dram_bytes_per_sample"]
         hit = [v for k, v in per.items() if kname in k]
@@ -285,7 +305,32 @@ def main():
     roofline = {"bound": "hbm", "achieved": kern[dom]["gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": kern[dom]["gbs"] / hbm, "traffic": traffic, "kernel": dom, "peak_source": peak_kind,
                 "bytes_per_sample": 16, "algorithmic_bytes_per_launch": 16 * kern[dom]["samples_per_launch"],
-                "kernels": kern, "fft_stage": fft_stage}
+                "kernels": kern, "stages_multi_kernel": stages, "fft_stage": fft_stage}
+
+    # ---------------- the opt-in single persistent kernel (DISPCORR_FUSED=1), timed the same way
+    alternatives = None
+    if n == (1 << 20) and os.environ.get("DISPCORR_FUSED") != "1":
+        old = os.environ.get("DISPCORR_FUSED")
+        os.environ["DISPCORR_FUSED"] = "1"
+        plan_f = dc.Plan(n, FS, 0.0, taps=taps, stream=stream)
+        if old is None:
+            del os.environ["DISPCORR_FUSED"]
+        else:
+            os.environ["DISPCORR_FUSED"] = old
+        for _ in range(2):
+            plan_f.correct(x, y, tec_r, alpha_r)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            f0.record(stream)
+            for _ in range(args.steps):
+                plan_f.correct(x, y, tec_r, alpha_r)
+            f1.record(stream)
+        f1.synchronize()
+        fms = max_over_ranks(f0.elapsed_time(f1), device="cuda")
+        alternatives = {"fused_single_kernel": {"value": pulses * n * args.steps / (fms / 1e3), "unit": UNIT,
+                                                "note": "opt-in DISPCORR_FUSED=1; not the default (slower)"}}
+        plan_f.close()
+        plan.correct(x, y, tec_r, alpha_r)  # leave y from the default path for the e2e check below
 
     # ---------------- end to end through the public host-buffer API (pinned host memory)
     e2e = None
@@ -333,6 +378,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "alternatives": alternatives,
         }
         print(json.dumps(line), flush=True)
     plan.close()

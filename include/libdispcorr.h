@@ -124,9 +124,10 @@ dc_status dc_plan_info(dc_plan_t plan, dc_plan_info_t *info);
  * the plan launches is bracketed by CUDA events on the plan's stream; dc_profile_read()
  * synchronises the stream and returns, per class, the launches, summed device milliseconds and
  * samples processed since the last reset.  Classes: DC_K_IONO_SMALL (regime-0 fused FFT ->
- * phase -> IFFT), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler). */
+ * phase -> IFFT), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler),
+ * DC_K_FUSED (the single persistent dc_correct kernel used for n = 2^20). */
 enum { DC_K_IONO_SMALL = 0, DC_K_FOURSTEP_A = 1, DC_K_FOURSTEP_B = 2, DC_K_FOURSTEP_C = 3, DC_K_DOPPLER = 4,
-       DC_K_CLASSES = 5 };
+       DC_K_FUSED = 5, DC_K_CLASSES = 6 };
 typedef struct {
   int64_t launches[DC_K_CLASSES];
   double ms[DC_K_CLASSES];

@@ -40,11 +40,11 @@ class DispCorrError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
-KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler")
+KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler", "fused")
 
 
 class Profile(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5), ("samples", ctypes.c_int64 * 5)]
+    _fields_ = [("launches", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6), ("samples", ctypes.c_int64 * 6)]
 
 
 class PlanInfo(ctypes.Structure):

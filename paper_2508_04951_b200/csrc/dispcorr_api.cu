@@ -78,6 +78,14 @@ struct dc_plan_s {
   cudaStream_t ws[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   bool pipeline = false;  // DISPCORR_PIPE=1 enables (measured slower with large chunks; kept for tuning)
+  // fused persistent dc_correct (n = 2^20): L2-sized groups through a ring of `fdepth` groups
+  // opt-in (DISPCORR_FUSED=1): measured 44.7 GS/s vs 55.6 for the multi-kernel path -- the stages
+  // are compute-bound, so saving the intermediate HBM round trips does not pay yet
+  bool fused = false;
+  int fpg = 1, fdepth = 8, flag = 2, fhints = 7;  // ring of fdepth groups; wavefront lag; L2 policy bits
+  float2 *fring = nullptr;
+  unsigned long long *fsync = nullptr;
+  int64_t fsync_groups = 0;
   // host-path buffers (lazily allocated)
   float2 *hin[2] = {nullptr, nullptr}, *hout[2] = {nullptr, nullptr};
   int64_t host_chunk = 0;
@@ -301,7 +309,9 @@ dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses,
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                       int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
-  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, ln.cap};
+  int cap = ln.cap;
+  if (const char *env = getenv("DISPCORR_DOP_CAP")) cap = atoi(env);  // tuning experiments only
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, cap};
   ProfScope ps(p, DC_K_DOPPLER, pulses * p->n, ln.st);
   DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
   return DC_OK;
@@ -495,6 +505,12 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     if ((s = upload(&p->gtab, g)) != DC_OK) return cleanup(s);
   }
   if (const char *env = getenv("DISPCORR_PIPE")) p->pipeline = atoi(env) != 0;
+  if (const char *env = getenv("DISPCORR_FUSED")) p->fused = atoi(env) != 0;
+  if (const char *env = getenv("DISPCORR_FUSED_PG")) p->fpg = std::max(1, atoi(env));
+  if (const char *env = getenv("DISPCORR_FUSED_LAG")) p->flag = std::max(1, atoi(env));
+  p->fdepth = 3 * p->flag + 2;
+  if (const char *env = getenv("DISPCORR_FUSED_DEPTH")) p->fdepth = std::max(3 * p->flag + 1, atoi(env));
+  if (const char *env = getenv("DISPCORR_FUSED_HINTS")) p->fhints = atoi(env);
   p->chunk = std::min<int64_t>(p->chunk, 65535);
   p->scratch_bytes = 0;  // chunk buffers are allocated on first use, sized to the batch (ensure_scratch)
   for (auto &slot : p->ring)
@@ -511,7 +527,8 @@ dc_status dc_plan_destroy(dc_plan_t p) {
   for (int i = 0; i < 2; ++i) {
     if (p->ws[i]) cudaStreamSynchronize(p->ws[i]);
   }
-  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab,
+  if (p->fsync) cudaFree(p->fsync);
+  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab, p->fring,
                     p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
   for (float2 *b : bufs)
     if (b) cudaFree(b);
@@ -597,6 +614,51 @@ dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   if ((s = stage_params(p, batch, tec, alpha, &pp, &slot, &mb)) != DC_OK) return s;
   const float2 *xp = (const float2 *)x;
   float2 *yp = (float2 *)y;
+  if (p->fused && p->log2n == 20 && p->regime == 1 && p->tw1024 && p->gtab && dc::doppler_path(mb) != 0) {
+    // one persistent kernel: groups of fpg pulses through an L2-sized ring (fused_correct.cu)
+    const int64_t ngroups = (batch + p->fpg - 1) / p->fpg;
+    if (!p->fring) {
+      if (cudaMalloc(&p->fring, (size_t)p->fpg * p->fdepth * p->n * sizeof(float2)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DC_ERR_OUT_OF_MEMORY, "fused ring buffer");
+      }
+    }
+    if (p->fsync_groups < ngroups) {
+      if (p->fsync) cudaFree(p->fsync);
+      p->fsync = nullptr;
+      if (cudaMalloc(&p->fsync, sizeof(unsigned long long) + 16 * (size_t)ngroups) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DC_ERR_OUT_OF_MEMORY, "fused scheduler state");
+      }
+      p->fsync_groups = ngroups;
+    }
+    unsigned long long *stats = nullptr;
+    const bool want_stats = getenv("DISPCORR_FUSED_STATS") != nullptr;  // tuning only: per-CTA cycle split
+    if (want_stats) {
+      if (cudaMalloc(&stats, 148 * 16 * 8) != cudaSuccess) return fail(DC_ERR_OUT_OF_MEMORY, "stats");
+      cudaMemsetAsync(stats, 0, 148 * 16 * 8, p->stream);
+    }
+    dc::FusedLaunch f{xp, yp, p->fring, batch, p->fpg, p->fdepth, p->flag, p->fhints, pp, p->tw1024, p->gtab, p->taps, p->fc / p->fs,
+                      p->fsync, stats, p->stream};
+    {
+      ProfScope ps(p, DC_K_FUSED, batch * p->n, p->stream);
+      DC_CUDA(dc::launch_fused_correct(f, mb), "fused_correct_kernel launch");
+    }
+    if (want_stats) {
+      unsigned long long h[148 * 16];
+      cudaMemcpyAsync(h, stats, sizeof h, cudaMemcpyDeviceToHost, p->stream);
+      cudaStreamSynchronize(p->stream);
+      cudaFree(stats);
+      double t[16] = {0};
+      for (int b = 0; b < 148; ++b)
+        for (int k = 0; k < 16; ++k) t[k] += (double)h[b * 16 + k] / 148.0;
+      fprintf(stderr,
+              "fused stats (mean cycles per CTA): wait_full %.0f  A %.0f  B %.0f  C %.0f  D %.0f  items %.0f+%.0f  "
+              "producer dep %.0f free %.0f\n",
+              t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[8], t[9]);
+    }
+    return release_slot(p, slot);
+  }
   const int64_t nchunks = (batch + p->chunk - 1) / p->chunk;
   const bool pipe = nchunks > 1 && !p->prof && p->pipeline;
   if (pipe && (s = fork(p)) != DC_OK) return s;

@@ -79,7 +79,9 @@ __device__ __forceinline__ void tap_w(float u, int m, float S, float Cc, float &
 // One doppler tile: R = 9 outputs per thread from the staged span sb (x[Bcta + i] = sb[i]),
 // carrier rotation, then a coalesced store of the tile's M outputs through `ob` (one barrier
 // inside; callers add the trailing barrier before ob / sb are reused).
-template <bool SECOND, int WT>
+// BAR = 0: the whole CTA (kDopT threads) computes the tile; BAR > 0: named barrier BAR over the
+// kDopT threads 0 .. kDopT-1 (the consumer warps of a warp-specialised kernel).
+template <bool SECOND, int WT, int BAR = 0>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
                                                  double carrier) {
@@ -228,7 +230,11 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   }
 #pragma unroll
   for (int r = 0; r < kDopR; ++r) ob[tid * kDopR + r] = acc[r];
-  __syncthreads();
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"n"(BAR), "n"(kDopT) : "memory");
+  }
   {
     float2 *yp = y + cur.pulse * n + cur.m0;
     const int64_t valid = min((int64_t)kDopM, n - cur.m0);

@@ -21,7 +21,7 @@ tot = e0.elapsed_time(e1) / 2
 p.profile_enable(True)
 p.correct(x, y, tec, alpha)
 pr = p.profile_read()
-out = {"lib": os.path.basename(dc.library_path()), "log2n": log2n, "pulses": pulses, "ms_per_call": tot,
+out = {"lib": os.path.basename(dc.library_path()), "fused_env": os.environ.get("DISPCORR_FUSED", "1"), "pg": os.environ.get("DISPCORR_FUSED_PG"), "depth": os.environ.get("DISPCORR_FUSED_DEPTH"), "log2n": log2n, "pulses": pulses, "ms_per_call": tot,
        "GS/s": pulses * n / tot / 1e6}
 for k, v in pr.items():
     if v["launches"]:
