@@ -181,6 +181,50 @@ int orc_iono(int64_t n, double fs, double fc, double tec, int method, const doub
 }
 
 /* ---------------------------------------------------------------------------
+ * Pulse compression after the ionospheric correction (the
+ * paper's pulse-compression path, fig:pulse_compression_path P:L246-251, whose
+ * headline timing is "during pulse compression").  The corrected pulse
+ * y = iono(x) (Eq. 15) is matched-filtered against a reference r_0 .. r_{L-1}
+ * (L <= n), circularly over the n-sample window (reading R16):
+ *   z_m = sum_{s=0}^{L-1} y_{(s+m) mod n} conj(r_s)
+ * i.e. the circular cross-correlation, which equals IDFT_n(Y_k conj(R_k)) with
+ * R = DFT_n of r zero-padded to n.  Written here as the direct sum (the
+ * definition), for the outputs listed in idx (all n when idx == NULL).
+ * ------------------------------------------------------------------------- */
+int orc_correlate(int64_t n, const double *y, int64_t L, const double *r, int64_t nidx,
+                  const int64_t *idx, double *z) {
+  if (n < 1 || L < 1 || L > n) return -1;
+  const int64_t cnt = idx ? nidx : n;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t i = 0; i < cnt; ++i) {
+    const int64_t m = idx ? idx[i] : i;
+    double ar = 0.0, ai = 0.0;
+    for (int64_t s = 0; s < L; ++s) {
+      const int64_t t = (s + m) % n;
+      const double yr = y[2 * t], yi = y[2 * t + 1], rr = r[2 * s], ri = r[2 * s + 1];
+      ar += yr * rr + yi * ri; /* y conj(r) */
+      ai += yi * rr - yr * ri;
+    }
+    z[2 * i] = ar;
+    z[2 * i + 1] = ai;
+  }
+  return 0;
+}
+
+int orc_compress(int64_t n, double fs, double fc, double tec, const double *x, int64_t L,
+                 const double *r, int64_t nidx, const int64_t *idx, double *z) {
+  if (n < 1 || L < 1 || L > n) return -1;
+  double *y = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+  if (!y) return -2;
+  int rc = orc_iono(n, fs, fc, tec, (n & (n - 1)) ? 1 : 0, x, y);
+  if (rc == 0) rc = orc_correlate(n, y, L, r, nidx, idx, z);
+  free(y);
+  return rc;
+}
+
+/* ---------------------------------------------------------------------------
  * Doppler time-dilation correction by windowed Whittaker-Shannon
  * interpolation, Eq. 16 restricted to a window of W samples
  * (Alg. 1, window P:L533).  Resampling onto t/alpha

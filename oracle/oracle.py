@@ -62,6 +62,8 @@ def _load():
         lib.orc_doppler_exact.restype = i32
         lib.orc_doppler_exact.argtypes = [i64, d, d, d, p, p]
         lib.orc_run_batch.restype = i32
+        lib.orc_correlate.argtypes = [i64, p, i64, p, i64, p, p]
+        lib.orc_compress.argtypes = [i64, d, d, d, p, i64, p, i64, p, p]
         lib.orc_run_batch.argtypes = [i32, i64, i64, d, d, i32, p, p, p, p, i32, i32]
         lib.orc_max_threads.restype = i32
         _lib = lib
@@ -162,6 +164,32 @@ def doppler_exact(x, fs: float, fc: float, alpha: float) -> np.ndarray:
 def correct(x, W: int, fs: float, fc: float, tec: float, alpha: float) -> np.ndarray:
     """dc_correct = doppler(iono(x)), iono first (reading R7)."""
     return doppler(iono(x, fs, fc, tec), W, fs, fc, alpha)
+
+
+def correlate(y, r, idx=None) -> np.ndarray:
+    """Circular matched filter z_m = sum_s y[(s+m) mod n] conj(r_s) (direct sum), at outputs idx."""
+    y, r = _c128(y), _c128(r)
+    n, L = y.size, r.size
+    ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
+    z = np.empty(n if ix is None else ix.size, dtype=np.complex128)
+    rc = _load().orc_correlate(n, _ptr(y), L, _ptr(r), 0 if ix is None else ix.size,
+                               None if ix is None else _ptr(ix), _ptr(z))
+    if rc:
+        raise RuntimeError(f"orc_correlate failed ({rc})")
+    return z
+
+
+def compress(x, fs: float, fc: float, tec: float, r, idx=None) -> np.ndarray:
+    """Pulse compression of the iono-corrected pulse: correlate(iono(x), r) (reading R16)."""
+    x, r = _c128(x), _c128(r)
+    n, L = x.size, r.size
+    ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
+    z = np.empty(n if ix is None else ix.size, dtype=np.complex128)
+    rc = _load().orc_compress(n, fs, fc, tec, _ptr(x), L, _ptr(r), 0 if ix is None else ix.size,
+                              None if ix is None else _ptr(ix), _ptr(z))
+    if rc:
+        raise RuntimeError(f"orc_compress failed ({rc})")
+    return z
 
 
 STAGES = {"iono": 1, "doppler": 2, "correct": 3}

@@ -343,3 +343,83 @@ def test_batch_entry_matches_single_and_is_thread_independent():
         assert np.array_equal(y1[p], ref)
     yi = O.run_batch("iono", x, fs, 0.0, 16, tec, alpha)
     assert np.array_equal(yi[2], O.iono(x[2].astype(np.complex128), fs, 0.0, tec[2]))
+
+
+# --------------------------------------------------------------------------- pulse compression (NEXT-2, reading R16)
+def test_correlate_autocorrelation_peak_is_energy():
+    # matched filter of the reference itself: z_0 = sum |r|^2 (closed form), |z_m| <= z_0 (Cauchy-Schwarz)
+    n, Lr = 512, 200
+    r = synth.complex_gaussian(Lr, seed=11)
+    x = np.zeros(n, complex)
+    x[:Lr] = r
+    z = O.correlate(x, r)
+    e = np.sum(np.abs(r) ** 2)
+    assert abs(z[0] - e) < 1e-12 * e
+    assert np.all(np.abs(z) <= e * (1 + 1e-12))
+    assert np.argmax(np.abs(z)) == 0
+
+
+@pytest.mark.parametrize("d", [0, 1, 37, 511])
+def test_correlate_delayed_copy_peaks_at_delay(d):
+    # x = r delayed circularly by d samples -> z_d = energy, argmax = d (sign of the lag fixed)
+    n, Lr = 512, 64
+    r = synth.complex_gaussian(Lr, seed=12)
+    x = np.zeros(n, complex)
+    x[(np.arange(Lr) + d) % n] = r
+    z = O.correlate(x, r)
+    assert np.argmax(np.abs(z)) == d
+    assert abs(z[d] - np.sum(np.abs(r) ** 2)) < 1e-12 * np.sum(np.abs(r) ** 2)
+
+
+def test_correlate_matches_numpy_fft_correlation():
+    # independent library: IDFT(DFT(y) conj(DFT(r_padded))) with numpy.fft; also sampled outputs
+    n, Lr = 256, 100
+    y = synth.complex_gaussian(n, seed=13)
+    r = synth.complex_gaussian(Lr, seed=14)
+    rp = np.zeros(n, complex)
+    rp[:Lr] = r
+    ref = np.fft.ifft(np.fft.fft(y) * np.conj(np.fft.fft(rp)))
+    z = O.correlate(y, r)
+    assert np.max(np.abs(z - ref)) < 1e-12 * np.max(np.abs(ref))
+    idx = np.array([0, 5, 255, 128])
+    assert np.array_equal(O.correlate(y, r, idx), z[idx])
+
+
+def test_compress_is_correlation_of_corrected_pulse():
+    # compress(distort(x)) = correlate(x, r): the Eq. 15 correction undoes Eq. 14 before matching
+    n = 1024
+    x = synth.complex_gaussian(n, seed=15)
+    r = synth.complex_gaussian(300, seed=16)
+    fs, fc, tec = 51.2e6, 422e6, 1e18
+    xd = O.iono(x, fs, fc, tec, distort=True)
+    z = O.compress(xd, fs, fc, tec, r)
+    ref = O.correlate(x, r)
+    assert np.max(np.abs(z - ref)) < 1e-10 * np.max(np.abs(ref))
+    # tec = 0: compress is the plain matched filter
+    assert np.max(np.abs(O.compress(x, fs, fc, 0.0, r) - ref)) < 1e-12 * np.max(np.abs(ref))
+
+
+def test_compress_lfm_peak_sidelobe_textbook():
+    # large time-bandwidth LFM (TB = 18 MHz x 100 us = 1800): compressed peak = energy at lag 0 and
+    # the first sidelobe sits near the sinc value -13.26 dB (textbook pulse-compression result);
+    # a missing conj gives no compression at all
+    fs, n = 204.8e6, 1 << 15
+    T, B = 100e-6, 18e6
+    ns = int(round(T * fs))
+    t = np.arange(ns) / fs
+    r = np.exp(1j * np.pi * (B / T) * (t - T / 2) ** 2)
+    x = np.zeros(n, complex)
+    x[:ns] = r
+    z = np.abs(O.compress(x, fs, 0.0, 0.0, r))
+    assert np.argmax(z) == 0 and abs(z[0] - ns) < 1e-9 * ns
+    zz = np.concatenate([z[n // 2:], z[:n // 2]])
+    c = n // 2
+    # walk out of the main lobe to the first null, then take the highest sidelobe near it
+    k = c + 1
+    while zz[k + 1] < zz[k]:
+        k += 1
+    side = np.max(zz[k:k + int(3 * fs / B)])
+    sll = 20 * np.log10(side / zz[c])
+    assert -13.8 < sll < -12.8
+    wrong = np.abs(np.fft.ifft(np.fft.fft(x) * np.fft.fft(np.pad(r, (0, n - ns)))))
+    assert np.max(wrong) < 0.2 * ns

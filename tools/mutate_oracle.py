@@ -22,6 +22,9 @@ MUTANTS = {
     "sinc missing pi": ("return sin(ORC_PI * d) / (ORC_PI * d);", "return sin(ORC_PI * d) / (d);"),
     "conj multiply": ("X[2 * k + 1] = xr * s + xi * c;", "X[2 * k + 1] = -xr * s + xi * c;"),
     "drop last sample": ("if (k < 0 || k >= n) continue;", "if (k < 0 || k >= n - 1) continue;"),
+    "correlate without conj": ("ar += yr * rr + yi * ri; /* y conj(r) */\n      ai += yi * rr - yr * ri;", "ar += yr * rr - yi * ri;\n      ai += yi * rr + yr * ri;"),
+    "correlate lag sign": ("const int64_t t = (s + m) % n;", "const int64_t t = (s - m + n) % n;"),
+    "compress skips iono": ("int rc = orc_iono(n, fs, fc, tec, (n & (n - 1)) ? 1 : 0, x, y);", "int rc = 0; memcpy(y, x, sizeof(double) * 2 * (size_t)n);"),
     "no u==0 sinc case": ("if (d == 0.0) return 1.0;\n  if (d == floor(d)) return 0.0;", "if (d == 0.0) return 1.0;"),
 }
 
