@@ -56,8 +56,8 @@ static size_t warp_row_smem(int log2n, int H, bool outer) {
   return RowCfg<DC_ROW_NW, kRowStage>::elems(outer, log2n, H) * sizeof(float2);
 }
 static size_t warp_col_smem(int log2n, int H, bool outer) {
-  size_t e = (size_t)2 * 1024 * 8 + (size_t)kWW * (kWPad + 32) + 1024;
-  if (outer) e += (size_t)(1 << H) + (1 << (log2n - H));
+  (void)outer, (void)log2n, (void)H;  // outer twiddles come from twn(): no table staged
+  const size_t e = (size_t)2 * 1024 * 8 + (size_t)kWW * (kWPad + 32) + 1024;
   return e * sizeof(float2) + 2 * sizeof(uint64_t) + 1024;  // + mbarriers, alignment slack
 }
 template <class K>

@@ -40,11 +40,6 @@ __device__ __forceinline__ void wfft1024(float2 (&v)[32], float2 *__restrict__ w
   DFT<32, INV>::run(v);
 }
 
-// outer-twiddle helper: per-warp table P[s] = w_n^(32 a s mod n), s = 0..31 (one exact
-// two-level lookup per lane), so that w_n^(a (lane + 32 s)) = w_n^(a lane) * P[s].
-__device__ __forceinline__ float2 tw2(uint32_t m, int H, uint32_t hmask, const float2 *Th, const float2 *Tl) {
-  return cmul(Th[m >> H], Tl[m & hmask]);
-}
 // w_n^m = exp(-2 pi i m / n) for 0 <= m < n = 2^log2n via sincospif of the exact FP32 argument
 // 2 m / n (m < 2^24 is exact in FP32): ~1 ulp, no table, no shared-memory bank conflicts.
 __device__ __forceinline__ float2 twn(uint32_t m, int log2n) {
@@ -81,7 +76,8 @@ template <int NW, bool STAGE>
 struct RowCfg {
   static constexpr int STG = STAGE ? 2048 : 0;  // staging per warp (float2): Z row + g row
   static __host__ __device__ constexpr size_t elems(bool outer, int log2n, int H) {
-    return (size_t)NW * (STG + kWPad + 32) + 1024 + (outer ? ((size_t)(1 << H) + (1 << (log2n - H))) : 0);
+    // (outer twiddles come from twn(), so no outer-twiddle table is staged)
+    return (void)outer, (void)log2n, (void)H, (size_t)NW * (STG + kWPad + 32) + 1024;
   }
 };
 
@@ -95,12 +91,9 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
   float2 *wk = sm + NW * CFG::STG + warp * kWPad;            // per-warp exchange
   float2 *Pw = sm + NW * (CFG::STG + kWPad) + warp * 32;     // per-warp outer-twiddle powers
   float4 *Tw = reinterpret_cast<float4 *>(sm + NW * (CFG::STG + kWPad + 32));
-  float2 *Th = reinterpret_cast<float2 *>(Tw) + 1024;
-  const int H = a.H;
   const int log2n = a.log2n;
   const int n = 1 << log2n;
-  float2 *Tl = Th + (MODE == MODE_ROWB ? (n >> H) : 0);
-  const uint32_t nmask = (uint32_t)n - 1u, hmask = (1u << H) - 1u;
+  const uint32_t nmask = (uint32_t)n - 1u;
   const int P1 = log2n - 10;
   const int64_t rows_per_pulse = (MODE == MODE_ROWB) ? ((int64_t)1 << P1) : 1;
   const int64_t total = a.pulses * rows_per_pulse;
@@ -108,9 +101,6 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
 
   // tables (once per CTA)
   for (int i = threadIdx.x; i < 512; i += NW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  (void)Th;
-  (void)Tl;
-  (void)hmask;  // outer twiddles come from twn() (sincospif), not the two-level table
   auto row_ptr = [&](const float2 *base, int64_t it) {
     const int64_t p = it / rows_per_pulse, k1 = it - p * rows_per_pulse;
     return base + p * a.pulse_stride + k1 * 1024;
@@ -226,19 +216,15 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a,
   float2 *wk = wkall + warp * kWPad;
   float2 *Pw = wkall + kWW * kWPad + warp * 32;
   float4 *Tw = reinterpret_cast<float4 *>(wkall + kWW * (kWPad + 32));
-  float2 *Th = reinterpret_cast<float2 *>(Tw) + 1024;
-  const int H = a.H;
   const int log2n = a.log2n;
   const int n = 1 << log2n;
-  float2 *Tl = Th + (!INV ? (n >> H) : 0);
-  const uint32_t nmask = (uint32_t)n - 1u, hmask = (1u << H) - 1u;
+  const uint32_t nmask = (uint32_t)n - 1u;
   const int n2 = n >> 10;
   const int64_t tiles_per_pulse = n2 / kWW;
   const int64_t total = a.pulses * tiles_per_pulse;
 
   for (int i = tid; i < 512; i += kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  (void)hmask;  // outer twiddles come from twn() (sincospif), not the two-level table
-  uint64_t *bars = reinterpret_cast<uint64_t *>(Tl + (!INV ? (1 << H) : 0));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(Tw + 512);  // outer twiddles come from twn(): no table
   auto stage = [&](int64_t it, float2 *stg, uint64_t *bar) {  // thread 0 only
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
     fence_proxy_async();
