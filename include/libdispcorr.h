@@ -86,6 +86,24 @@ dc_status dc_iono(dc_plan_t plan, void *x, int64_t batch, const double *tec);
  * Used to synthesise dispersed echoes and the matched-filter reference. */
 dc_status dc_iono_distort(dc_plan_t plan, void *x, int64_t batch, const double *tec);
 
+/* Matched-filter reference for dc_compress (the paper's pulse-compression path,
+ * fig:pulse_compression_path P:L246-251; "46 us ... during pulse compression").
+ * r: device float2[L], 1 <= L <= n, the transmitted reference r_0 .. r_{L-1}; it is
+ * zero-padded to n and its DFT R_k is computed on the device and kept (conjugated) in
+ * the plan (8n bytes), replacing any earlier reference.  r may be reused as soon as
+ * the plan's stream has passed this call.  Supported for n = 2^10 and n = 2^17 .. 2^21
+ * (the warp-level row-FFT regimes); other n return DC_ERR_INVALID_VALUE. */
+dc_status dc_set_reference(dc_plan_t plan, const void *r, int64_t L);
+
+/* Pulse compression after the ionospheric correction (reading R16):
+ *   z[p][m] = sum_{s=0}^{L-1} y[p][(s + m) mod n] conj(r_s),   y[p] = dc_iono(x[p], tec[p]),
+ * i.e. z = F^-1[ F(x) e^{-i 2 pi nu_k} conj(R_k) ] -- the conj(R_k) multiply is fused into the
+ * Eq. 15 phase step, so compression costs no HBM bytes beyond dc_iono's.
+ * x, z: device float2[batch][n]; z == x (in place) or z disjoint from x (else
+ * DC_ERR_ALIASING).  tec: host double[batch] as dc_iono.  DC_ERR_INVALID_VALUE when no
+ * reference has been set or n is unsupported (see dc_set_reference). */
+dc_status dc_compress(dc_plan_t plan, const void *x, void *z, int64_t batch, const double *tec);
+
 /* Doppler correction: y[p][m] = e^{-i 2 pi fc (1 - beta) m / fs} *
  *   sum_{k : -W/2 < k - t_m <= W/2, 0 <= k < n} x[p][k] sinc(t_m - k),   t_m = m * beta,
  *   beta = 1/alpha[p] (binary64), sinc(d) = sin(pi d)/(pi d), sinc(0) = 1   (Eq. 16 windowed;

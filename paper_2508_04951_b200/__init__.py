@@ -11,6 +11,7 @@ raised.
     plan.iono(x, tec)                 # x: torch.complex64 [batch, n] on cuda, in place (Eq. 15)
     plan.doppler(x, y, alpha)         # y = resampled onto t/alpha (Eq. 16, windowed)
     plan.correct(x, y, tec, alpha)    # both stages, iono first
+    plan.set_reference(r); plan.compress(x, z, tec)   # iono correction + matched filter (fused)
 """
 from __future__ import annotations
 
@@ -75,6 +76,8 @@ def load():
         "dc_iono": ([p, p, i64, pd], i32),
         "dc_iono_distort": ([p, p, i64, pd], i32),
         "dc_doppler": ([p, p, p, i64, pd], i32),
+        "dc_set_reference": ([p, p, i64], i32),
+        "dc_compress": ([p, p, p, i64, pd], i32),
         "dc_correct": ([p, p, p, i64, pd, pd], i32),
         "dc_correct_host": ([p, p, p, i64, pd, pd], i32),
         "dc_plan_info": ([p, ctypes.POINTER(PlanInfo)], i32),
@@ -216,6 +219,25 @@ class Plan:
         tec_a, pt = _f64(tec, batch, "tec")
         _check(load().dc_iono_distort(self._h, px, batch, pt))
         return x
+
+    def set_reference(self, r):
+        """Matched-filter reference r (complex64 CUDA tensor of L <= n samples) for compress()."""
+        import torch
+        if not isinstance(r, torch.Tensor) or r.dtype != torch.complex64 or not r.is_cuda or not r.is_contiguous():
+            raise TypeError("r must be a contiguous complex64 CUDA tensor")
+        _check(load().dc_set_reference(self._h, ctypes.c_void_p(r.data_ptr()), int(r.numel())))
+        self._ref = r  # keep alive until the plan stream has consumed it
+        return self
+
+    def compress(self, x, z, tec):
+        """z = circular matched filter of iono(x) against the reference (z may be x)."""
+        px, batch = _dev_ptr(x, "x", self.n)
+        pz, bz = _dev_ptr(z, "z", self.n)
+        if bz != batch:
+            raise ValueError("x and z batch sizes differ")
+        tec_a, pt = _f64(tec, batch, "tec")
+        _check(load().dc_compress(self._h, px, pz, batch, pt))
+        return z
 
     def doppler(self, x, y, alpha):
         """Windowed-sinc resampling of x onto t/alpha into y (distinct buffers)."""

@@ -37,8 +37,12 @@ struct IonoSmallArgs {
   const float2 *tw1024;  // 1024-point pass-2 table for the warp-level kernels (n = 1024), or null
   int grid_cap;          // max CTAs of the persistent grid (0: one wave of the whole GPU)
   const float2 *gtab;    // per-bin 1/f_k FP32 pairs for the warp-level kernel, or null
+  const float2 *ref;     // var 2: conj reference spectrum (natural order), else null
+  float2 *ref_out;       // var 3: conj spectrum output, else null
 };
-cudaError_t launch_iono_small(const IonoSmallArgs &a, bool distort);
+// var: 0 Eq. 15 correction, 1 Eq. 14 distortion, 2 correction + matched filter (conj(R_k) table `ref`),
+// 3 forward spectrum of one pulse stored conjugated to `ref_out` (warp-level regimes only for 2, 3)
+cudaError_t launch_iono_small(const IonoSmallArgs &a, int var);
 
 struct FourStepArgs {
   const float2 *src;  // pass A input (pulse-major, pulse_stride apart)
@@ -57,11 +61,14 @@ struct FourStepArgs {
   const float2 *tw1024;       // 1024-point pass-2 table for the warp-level kernels, or null
   int grid_cap;               // max CTAs of the persistent grid (0: one wave of the whole GPU)
   const float2 *gtab;         // per-bin 1/f_k FP32 pairs (row layout) for the warp-level row kernel
+  const float2 *ref;          // var 2: conj reference spectrum in the row layout of gtab, else null
+  float2 *ref_out;            // var 3: conj spectrum output (row layout), else null
 };
 // offset (float2 entries) of the NS = 32 section inside the P = 10, radix-32 forward pass table
 int tw1024_offset();
-// pass 0 = A (columns, forward), 1 = B (rows, phase), 2 = C (columns, inverse)
-cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, bool distort);
+// pass 0 = A (columns, forward), 1 = B (rows, phase), 2 = C (columns, inverse); var as launch_iono_small
+// (var 3 runs passes A and B only)
+cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, int var);
 
 struct DopplerArgs {
   const float2 *x;

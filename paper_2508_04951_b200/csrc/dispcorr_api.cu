@@ -70,6 +70,8 @@ struct dc_plan_s {
   float2 *tw1f = nullptr, *tw1i = nullptr, *tw2f = nullptr, *tw2i = nullptr, *twh = nullptr, *twl = nullptr;
   const float2 *tw1024 = nullptr;  // radix-32 x 32 pass-2 table inside one of the tables above
   float2 *gtab = nullptr;          // per-bin 1/f_k as FP32 pairs, in the layout the warp row kernel reads
+  float2 *ref = nullptr;           // conj(R_k) of the matched-filter reference (dc_set_reference), gtab layout
+  bool ref_set = false;
   float2 *scratch = nullptr;  // chunk * n samples
   float2 *scratch2 = nullptr;  // second chunk buffer (two chunks in flight on the internal streams)
   int64_t scratch_bytes = 0;
@@ -270,13 +272,15 @@ struct Lane {
 };
 
 // ---- stage launchers (no validation) -----------------------------------------------------------
+// var: 0 Eq. 15, 1 Eq. 14, 2 Eq. 15 + matched filter, 3 conj reference spectrum into p->ref
 dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
-                   int64_t pulse_base, bool distort, Lane ln) {
+                   int64_t pulse_base, int var, Lane ln) {
   if (p->regime == 0) {
-    dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp + pulse_base, p->tw_small_f, p->tw_small_i,
-                        p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab};
+    dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp ? pp + pulse_base : nullptr, p->tw_small_f, p->tw_small_i,
+                        p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab, p->ref,
+                        var == 3 ? p->ref : nullptr};
     ProfScope ps(p, DC_K_IONO_SMALL, pulses * p->n, ln.st);
-    DC_CUDA(dc::launch_iono_small(a, distort), "iono_small_kernel launch");
+    DC_CUDA(dc::launch_iono_small(a, var), "iono_small_kernel launch");
     return DC_OK;
   }
   dc::FourStepArgs a{};
@@ -300,11 +304,18 @@ dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses,
   a.tw1024 = p->tw1024;
   a.grid_cap = ln.cap;
   a.gtab = p->gtab;
-  for (int pass = 0; pass < 3; ++pass) {
+  a.ref = p->ref;
+  a.ref_out = (var == 3) ? p->ref : nullptr;
+  for (int pass = 0; pass < (var == 3 ? 2 : 3); ++pass) {
     ProfScope ps(p, DC_K_FOURSTEP_A + pass, pulses * p->n, ln.st);
-    DC_CUDA(dc::launch_iono_fourstep_pass(a, pass, distort), "four-step kernel launch");
+    DC_CUDA(dc::launch_iono_fourstep_pass(a, pass, var), "four-step kernel launch");
   }
   return DC_OK;
+}
+
+// pulse compression (var 2/3) runs on the warp-level row kernel: n = 2^10 or 2^17 .. 2^21
+bool compress_supported(const dc_plan_s *p) {
+  return p->tw1024 && p->gtab && ((p->regime == 0 && p->log2n == 10) || (p->regime == 1 && p->P2 == 10));
 }
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
@@ -358,17 +369,28 @@ dc_status ensure_scratch(dc_plan_s *p, int64_t batch) {
   return DC_OK;
 }
 
-dc_status iono_common(dc_plan_t p, void *x, int64_t batch, const double *tec, bool distort) {
+// src -> dst (dst == src: in place); var as run_iono (0, 1 or 2)
+dc_status iono_common(dc_plan_t p, const void *x, void *z, int64_t batch, const double *tec, int var) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
   dc_status s;
   if ((s = check_batch(batch)) != DC_OK) return s;
   if ((s = check_device_ptr(p, x, "x")) != DC_OK) return s;
+  if (z != x) {
+    if ((s = check_device_ptr(p, z, "z")) != DC_OK) return s;
+    if ((s = check_overlap(x, z, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
+  }
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
+  if (var == 2) {
+    if (!compress_supported(p))
+      return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^17 .. 2^21 (plan n = %lld)", (long long)p->n);
+    if (!p->ref_set) return fail(DC_ERR_INVALID_VALUE, "no matched-filter reference: call dc_set_reference first");
+  }
   DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
   PulseParams *pp;
   ParamSlot *slot;
   if ((s = stage_params(p, batch, tec, nullptr, &pp, &slot, nullptr)) != DC_OK) return s;
-  float2 *xp = (float2 *)x;
+  const float2 *xp = (const float2 *)x;
+  float2 *zp = (float2 *)z;
   const int64_t step = (p->regime == 0) ? std::min<int64_t>(batch, 1ll << 30) : p->chunk;
   const int64_t nchunks = (batch + step - 1) / step;
   const bool pipe = nchunks > 1 && !p->prof && p->pipeline;
@@ -376,7 +398,7 @@ dc_status iono_common(dc_plan_t p, void *x, int64_t batch, const double *tec, bo
   for (int64_t b0 = 0, i = 0; b0 < batch; b0 += step, ++i) {
     const int64_t nb = std::min(step, batch - b0);
     const Lane ln = pipe ? Lane{p->ws[i & 1], (p->sm_count + 1) / 2} : Lane{p->stream, 0};
-    if ((s = run_iono(p, xp + b0 * p->n, xp + b0 * p->n, nb, pp, b0, distort, ln)) != DC_OK) return s;
+    if ((s = run_iono(p, xp + b0 * p->n, zp + b0 * p->n, nb, pp, b0, var, ln)) != DC_OK) return s;
   }
   if (pipe && (s = join(p)) != DC_OK) return s;
   return release_slot(p, slot);
@@ -528,7 +550,7 @@ dc_status dc_plan_destroy(dc_plan_t p) {
     if (p->ws[i]) cudaStreamSynchronize(p->ws[i]);
   }
   if (p->fsync) cudaFree(p->fsync);
-  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab, p->fring,
+  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab, p->fring, p->ref,
                     p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
   for (float2 *b : bufs)
     if (b) cudaFree(b);
@@ -568,11 +590,37 @@ dc_status dc_sync(dc_plan_t p) {
 }
 
 dc_status dc_iono(dc_plan_t p, void *x, int64_t batch, const double *tec) {
-  return iono_common(p, x, batch, tec, false);
+  return iono_common(p, x, x, batch, tec, 0);
 }
 
 dc_status dc_iono_distort(dc_plan_t p, void *x, int64_t batch, const double *tec) {
-  return iono_common(p, x, batch, tec, true);
+  return iono_common(p, x, x, batch, tec, 1);
+}
+
+dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  dc_status s;
+  if (!compress_supported(p))
+    return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^17 .. 2^21 (plan n = %lld)", (long long)p->n);
+  if (L < 1 || L > p->n) return fail(DC_ERR_INVALID_VALUE, "reference length L = %lld must be in [1, n = %lld]", (long long)L, (long long)p->n);
+  if ((s = check_device_ptr(p, r, "r")) != DC_OK) return s;
+  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  if (!p->ref && cudaMalloc(&p->ref, (size_t)p->n * sizeof(float2)) != cudaSuccess) {
+    cudaGetLastError();
+    p->ref = nullptr;
+    return fail(DC_ERR_OUT_OF_MEMORY, "reference spectrum table");
+  }
+  if ((s = ensure_scratch(p, 1)) != DC_OK) return s;
+  // zero-padded reference in the chunk buffer, then its forward DFT stored conjugated (var 3)
+  DC_CUDA(cudaMemsetAsync(p->scratch, 0, (size_t)p->n * sizeof(float2), p->stream), "cudaMemsetAsync");
+  DC_CUDA(cudaMemcpyAsync(p->scratch, r, (size_t)L * sizeof(float2), cudaMemcpyDeviceToDevice, p->stream), "cudaMemcpyAsync");
+  if ((s = run_iono(p, p->scratch, p->scratch, 1, nullptr, 0, 3, Lane{p->stream, 0})) != DC_OK) return s;
+  p->ref_set = true;
+  return DC_OK;
+}
+
+dc_status dc_compress(dc_plan_t p, const void *x, void *z, int64_t batch, const double *tec) {
+  return iono_common(p, x, z, batch, tec, 2);
 }
 
 dc_status dc_doppler(dc_plan_t p, const void *x, void *y, int64_t batch, const double *alpha) {

@@ -35,8 +35,11 @@ namespace dc {
 // Persistent, double-buffered pipeline: while the CTA computes tile i from one shared buffer,
 // the input span of tile i + gridDim.x streams into the other with cp.async (zero-filled).
 // WT > 0: the tap count W is a compile-time constant (fully unrolled tap loop); WT = 0: runtime W.
+#ifndef DC_DOP_MINB
+#define DC_DOP_MINB 2
+#endif
 template <bool SECOND, int WT>
-__global__ void __launch_bounds__(kDopT, 2)
+__global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
                         int buf_elems) {

@@ -10,7 +10,10 @@
 namespace dc {
 
 constexpr int kDopT = 256;  // threads per CTA
-constexpr int kDopR = 9;    // outputs per thread: odd, so lanes' windows (9 samples apart) hit distinct banks
+#ifndef DC_DOP_R
+#define DC_DOP_R 9
+#endif
+constexpr int kDopR = DC_DOP_R;  // outputs per thread: odd, so lanes' windows (R samples apart) hit distinct banks
 constexpr int kDopM = kDopT * kDopR;     // outputs per tile
 constexpr double kDopMaxDrift = 2.0e-3;  // max |beta - 1| * R / 2 for the fast path
 

@@ -74,17 +74,22 @@ static cudaError_t launch_persistent(K kern, size_t smem, int64_t total, const W
   kern<<<(unsigned)grid, nw * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
-static cudaError_t launch_warp_row(const WarpArgs &a, bool small, bool distort, cudaStream_t st, int cap) {
+template <int MODE>
+static cudaError_t launch_warp_row_mode(const WarpArgs &a, int var, size_t smem, int64_t items, cudaStream_t st, int cap) {
   constexpr int NW = DC_ROW_NW;
-  if (small) {
-    const size_t smem = warp_row_smem(a.log2n, a.H, false);
-    auto k = distort ? warp_row_kernel<MODE_SMALL, true, NW, kRowStage> : warp_row_kernel<MODE_SMALL, false, NW, kRowStage>;
-    return launch_persistent(k, smem, (a.pulses + NW - 1) / NW, a, st, cap, NW);
+  switch (var) {
+    case VAR_CORRECT: return launch_persistent(warp_row_kernel<MODE, VAR_CORRECT, NW, kRowStage>, smem, items, a, st, cap, NW);
+    case VAR_DISTORT: return launch_persistent(warp_row_kernel<MODE, VAR_DISTORT, NW, kRowStage>, smem, items, a, st, cap, NW);
+    case VAR_COMPRESS: return launch_persistent(warp_row_kernel<MODE, VAR_COMPRESS, NW, kRowStage>, smem, items, a, st, cap, NW);
+    case VAR_REFERENCE: return launch_persistent(warp_row_kernel<MODE, VAR_REFERENCE, NW, kRowStage>, smem, items, a, st, cap, NW);
+    default: return cudaErrorInvalidValue;
   }
+}
+static cudaError_t launch_warp_row(const WarpArgs &a, bool small, int var, cudaStream_t st, int cap) {
+  constexpr int NW = DC_ROW_NW;
+  if (small) return launch_warp_row_mode<MODE_SMALL>(a, var, warp_row_smem(a.log2n, a.H, false), (a.pulses + NW - 1) / NW, st, cap);
   const int64_t total_w = a.pulses << (a.log2n - 10);
-  const size_t smem = warp_row_smem(a.log2n, a.H, true);
-  auto k = distort ? warp_row_kernel<MODE_ROWB, true, NW, kRowStage> : warp_row_kernel<MODE_ROWB, false, NW, kRowStage>;
-  return launch_persistent(k, smem, (total_w + NW - 1) / NW, a, st, cap, NW);
+  return launch_warp_row_mode<MODE_ROWB>(a, var, warp_row_smem(a.log2n, a.H, true), (total_w + NW - 1) / NW, st, cap);
 }
 static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st, int cap) {
   const int64_t total = a.pulses * ((1ll << (a.log2n - 10)) / kWW);
@@ -96,19 +101,32 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
   const uint64_t strides[2] = {(uint64_t)n2 * sizeof(float2), (uint64_t)a.pulse_stride * sizeof(float2)};
   const uint32_t box[3] = {(uint32_t)kWW, 256, 1};
   if (!encode_tile_map(&smap, a.src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+#ifndef DC_COL_V1
+  const size_t smem2 = warp_col2_smem_bytes();
+  (void)smem;
+  auto kern = inv ? warp_col2_kernel<true> : warp_col2_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+#else
   auto kern = inv ? warp_col_kernel<true> : warp_col_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#endif
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWW * 32, smem);
+#ifndef DC_COL_V1
+  const size_t launch_smem = smem2;
+#else
+  const size_t launch_smem = smem;
+#endif
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWW * 32, launch_smem);
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  kern<<<(unsigned)grid, kWW * 32, smem, st>>>(a, smap);
+  kern<<<(unsigned)grid, kWW * 32, launch_smem, st>>>(a, smap);
   return cudaGetLastError();
 }
-static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr) {
+static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr,
+                          const float2 *ref = nullptr, float2 *ref_out = nullptr) {
   WarpArgs w{};
   w.src = t.src;
   w.dst = t.dst;
@@ -125,6 +143,8 @@ static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 
   w.fc = t.fc;
   w.scale = 1.0f / (float)(1 << t.log2n);
   w.gtab = gtab;
+  w.ref = ref;
+  w.ref_out = ref_out;
   return w;
 }
 // pass-2 section (NS = 32, R = 32) of the P = 10, E = 32 forward table: float4 [r/2][k] layout
@@ -138,7 +158,7 @@ static cudaError_t launch_small_p(const TileArgs &a, bool distort, cudaStream_t 
                  : launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, false>(a, total, st, cap);
 }
 
-cudaError_t launch_iono_small(const IonoSmallArgs &s, bool distort) {
+cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   TileArgs a{};
   a.src = s.xin;
   a.dst = s.xout;
@@ -152,7 +172,10 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, bool distort) {
   a.H = 0;
   a.fs_over_n = s.fs_over_n;
   a.fc = s.fc;
-  if (s.log2n == 10 && s.tw1024 && s.gtab) return launch_warp_row(warp_args(a, s.tw1024, s.gtab), true, distort, s.stream, s.grid_cap);
+  if (s.log2n == 10 && s.tw1024 && s.gtab)
+    return launch_warp_row(warp_args(a, s.tw1024, s.gtab, s.ref, s.ref_out), true, var, s.stream, s.grid_cap);
+  if (var != VAR_CORRECT && var != VAR_DISTORT) return cudaErrorInvalidValue;  // compress: warp-level regimes only
+  const bool distort = (var == VAR_DISTORT);
   switch (s.log2n) {
     case 1: return launch_small_p<1>(a, distort, s.stream, s.grid_cap);
     case 2: return launch_small_p<2>(a, distort, s.stream, s.grid_cap);
@@ -276,9 +299,13 @@ static cudaError_t launch_row(int P2, const TileArgs &a, cudaStream_t st, int ca
   }
 }
 
-cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, bool distort) {
+cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) {
   int P1, P2;
   fourstep_split(f.log2n, P1, P2);
+  // compress / reference need the warp-level row pass (N2 = 1024, n = 2^17 .. 2^21)
+  const bool warp_row = P2 == 10 && f.tw1024 && f.gtab;
+  if (var != VAR_CORRECT && var != VAR_DISTORT && !warp_row) return cudaErrorInvalidValue;
+  const bool distort = (var == VAR_DISTORT);
   TileArgs a{};
   a.pulses = f.pulses;
   a.pulse_stride = f.pulse_stride;
@@ -302,7 +329,8 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, bool dist
       a.dst = f.dst;
       a.twf = f.tw2f;
       a.twi = f.tw2i;
-      if (P2 == 10 && f.tw1024 && f.gtab) return launch_warp_row(warp_args(a, f.tw1024, f.gtab), false, distort, f.stream, f.grid_cap);
+      if (P2 == 10 && f.tw1024 && f.gtab)
+        return launch_warp_row(warp_args(a, f.tw1024, f.gtab, f.ref, f.ref_out), false, var, f.stream, f.grid_cap);
       return distort ? launch_row<true>(P2, a, f.stream, f.grid_cap) : launch_row<false>(P2, a, f.stream, f.grid_cap);
     case 2:
       a.src = f.dst;

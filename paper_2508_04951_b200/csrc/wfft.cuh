@@ -63,7 +63,16 @@ struct WarpArgs {
   double fs_over_n, fc;
   float scale;  // pass A: 1/n (inverse-transform normalisation folded into the outer twiddle)
   const float2 *gtab;  // per-bin 1/f_k FP32 pairs, row layout [k1][k2] (MODE_SMALL: natural order)
+  const float2 *ref;   // VAR_COMPRESS: conj(R_k) of the matched-filter reference, same layout as gtab
+  float2 *ref_out;     // VAR_REFERENCE: where conj(X_k) of the (single) input pulse is written
 };
+
+// What the row kernel does between its forward and inverse DFTs (bins X_k of one row):
+//   VAR_CORRECT   X_k e^{-i 2 pi nu_k}                 Eq. 15
+//   VAR_DISTORT   X_k e^{+i 2 pi nu_k}                 Eq. 14 forward model
+//   VAR_COMPRESS  X_k e^{-i 2 pi nu_k} conj(R_k)       Eq. 15 then the matched filter (reading R16)
+//   VAR_REFERENCE store conj(X_k) to ref_out, no inverse (builds the conj(R_k) table of VAR_COMPRESS)
+enum RowVar { VAR_CORRECT = 0, VAR_DISTORT = 1, VAR_COMPRESS = 2, VAR_REFERENCE = 3 };
 
 // MODE_ROWB: four-step pass B on rows k1 of Z (N2 = 1024).  MODE_SMALL: whole pulses of 1024.
 // NW warps per CTA.  STAGE: each warp prefetches its next row into a private shared buffer with
@@ -81,7 +90,7 @@ struct RowCfg {
   }
 };
 
-template <int MODE, bool DISTORT, int NW, bool STAGE>
+template <int MODE, int VAR, int NW, bool STAGE>
 __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) {
   using CFG = RowCfg<NW, STAGE>;
   extern __shared__ float4 smem4[];
@@ -151,25 +160,40 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
     // ---- Eq. 15 phase of bins k = k1 + N1 k2, k2 = lane + 32 s (MODE_SMALL: k = k2):
     // nu = nu_coef * g_k with g_k = 1/f_k from the plan table (0 for f_k <= 0, R3), FP32-pair math
     {
-      const PulseParams pr = a.pp[a.pulse_base + p];
       const float inv_n = (MODE == MODE_ROWB) ? 1.0f : 1.0f / (float)n;  // ROWB: 1/n applied in pass A
       if constexpr (STAGE) {
         cp_async_wait_1();  // this item's g row landed (the next Z row may still be in flight)
         __syncwarp();
       }
-      const float2 *grow = STAGE ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
+      if constexpr (VAR == VAR_REFERENCE) {
+        // reference spectrum: X_k of the zero-padded reference pulse, stored conjugated; ROWB undoes
+        // the 1/n that pass A folded in (exact: a power of two)
+        const float sc = (MODE == MODE_ROWB) ? (float)n : 1.0f;
 #pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        const float2 g = grow[lane + 32 * s];
-        const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
-        const float2 w = expm2pi(DISTORT ? -rf : rf);
-        v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
+        for (int s = 0; s < 32; ++s) a.ref_out[(int64_t)k1 * 1024 + lane + 32 * s] = make_float2(v[s].x * sc, -v[s].y * sc);
+      } else {
+        const PulseParams pr = a.pp[a.pulse_base + p];
+        const float2 *grow = STAGE ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
+        float2 rc[VAR == VAR_COMPRESS ? 32 : 1];
+        if constexpr (VAR == VAR_COMPRESS) {
+#pragma unroll
+          for (int s = 0; s < 32; ++s) rc[s] = __ldg(a.ref + (int64_t)k1 * 1024 + lane + 32 * s);
+        }
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+          const float2 g = grow[lane + 32 * s];
+          const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
+          const float2 w = expm2pi((VAR == VAR_DISTORT) ? -rf : rf);
+          v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
+          if constexpr (VAR == VAR_COMPRESS) v[s] = cmul(v[s], rc[s]);
+        }
       }
       if constexpr (STAGE) {
         __syncwarp();  // g staging consumed: prefetch the next g row
         if (it + G < total) stage_g(it + G);
         cp_async_commit_();
       }
+      if constexpr (VAR == VAR_REFERENCE) continue;
     }
 
     wfft1024<true>(v, wk, Tw, lane);
@@ -285,6 +309,84 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a,
       __stcg(reinterpret_cast<float4 *>(g + (int64_t)row * n2 + 2 * v4), make_float4(e0.x, e0.y, e1.x, e1.y));
     }
     __syncthreads();  // exchange buffers free before the next tile's FFT reuses them
+  }
+}
+
+// Column pass, default variant: ONE staging slot per CTA, reused in place as the 8 warps' padded
+// exchange space once the tile is in registers (the tile is 64 KiB, the exchange 8 x 1058
+// samples), so a CTA needs ~80 KiB and two CTAs (16 warps) share an SM: one CTA's TMA load and
+// stores overlap the other CTA's FFTs.  (warp_col_kernel above keeps two staging tiles plus
+// separate exchange buffers in one 196 KiB CTA: 8 warps per SM, latency-bound.)
+constexpr int kColSlot = ((kWW * kWPad * 8 + 1023) / 1024) * 1024 / 8;  // float2 elements
+__host__ __device__ constexpr size_t warp_col2_smem_bytes() {
+  return (size_t)kColSlot * 8 + kWW * 32 * 8 + 512 * 16 + 16 + 1024;
+}
+template <bool INV>
+__global__ void __launch_bounds__(kWW * 32, 2) warp_col2_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
+  extern __shared__ __align__(1024) float4 smem4[];
+  float2 *sb = reinterpret_cast<float2 *>(smem4);  // [1024][8] swizzled tile, then 8 exchange buffers
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  float2 *wk = sb + warp * kWPad;
+  float2 *Pw = sb + kColSlot + warp * 32;
+  float4 *Tw = reinterpret_cast<float4 *>(sb + kColSlot + kWW * 32);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(Tw + 512);
+  const int log2n = a.log2n;
+  const int n = 1 << log2n;
+  const uint32_t nmask = (uint32_t)n - 1u;
+  const int n2 = n >> 10;
+  const int64_t tiles_per_pulse = n2 / kWW;
+  const int64_t total = a.pulses * tiles_per_pulse;
+
+  for (int i = tid; i < 512; i += kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
+  auto stage = [&](int64_t it) {  // thread 0 only; every generic access to sb is ordered before it
+    const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, 1024 * 8 * sizeof(float2));
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tma_load_3d(sb + b * 256 * 8, &smap, (int)c0, b * 256, (int)p, bar);
+  };
+  int64_t it = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+    if (it < total) stage(it);
+  }
+  __syncthreads();
+  unsigned phase = 0u;
+  for (; it < total; it += gridDim.x) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    float2 v[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = sb[col_sw(lane + 32 * r, warp)];
+    __syncthreads();  // the whole tile is in registers: the slot becomes exchange space
+    const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
+    if constexpr (!INV) {
+      wfft1024<false>(v, wk, Tw, lane);
+      const uint32_t t2 = (uint32_t)(c0 + warp);
+      __syncwarp();
+      Pw[lane] = twn((32u * t2 * (uint32_t)lane) & nmask, log2n);
+      const float2 base = cscale(twn((t2 * (uint32_t)lane) & nmask, log2n), a.scale);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 32; ++s) v[s] = cmul(v[s], cmul(base, Pw[s]));
+    } else {
+      wfft1024<true>(v, wk, Tw, lane);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 32; ++s) wk[wpad(lane + 32 * s)] = v[s];
+    __syncthreads();
+    float2 *g = a.dst + p * a.pulse_stride + c0;
+#pragma unroll 4
+    for (int i = tid; i < 1024 * 4; i += kWW * 32) {
+      const int row = i >> 2, v4 = i & 3;
+      const float2 e0 = sb[(2 * v4) * kWPad + wpad(row)];
+      const float2 e1 = sb[(2 * v4 + 1) * kWPad + wpad(row)];
+      __stcg(reinterpret_cast<float4 *>(g + (int64_t)row * n2 + 2 * v4), make_float4(e0.x, e0.y, e1.x, e1.y));
+    }
+    __syncthreads();  // slot drained: load the next tile into it
+    if (tid == 0 && it + gridDim.x < total) stage(it + gridDim.x);
   }
 }
 

@@ -302,3 +302,73 @@ def test_fused_correct_matches_multi_kernel_path(dc, monkeypatch):
     idx = [0, 5, 10]
     ref = O.run_batch("correct", bank[np.arange(batch) % 4][idx], 2.048e9, 0.0, 32, tec[idx], alpha[idx])
     assert rel_l2(y1.cpu().numpy()[idx], ref).max() < TOL
+
+
+# ----------------------------------------------------------------------------- pulse compression (NEXT-2)
+def gpu_compress(dc, x, r, fs, fc, tec, inplace=False):
+    p = dc.Plan(x.shape[-1], fs, fc, taps=8)
+    p.set_reference(to_dev(r))
+    t = to_dev(x)
+    z = t if inplace else to_dev(np.zeros_like(x))
+    p.compress(t, z, tec)
+    return from_dev(z)
+
+
+@pytest.mark.parametrize("log2n,L", [(10, 300), (10, 1024), (17, 8192), (18, 1000), (21, 4096)])
+def test_compress_vs_oracle(dc, log2n, L):
+    # z = circular matched filter of iono(x) against r (oracle: the direct-sum definition)
+    n = 1 << log2n
+    rng = np.random.default_rng(log2n + L)
+    r = (rng.standard_normal(L) + 1j * rng.standard_normal(L)).astype(np.complex64)
+    x = synth.complex_gaussian(n, seed=200 + log2n, batch=2).astype(np.complex64)
+    tec = np.array([1e18, 0.0])
+    fs, fc = (2.048e9, 0.0) if log2n != 18 else (204.8e6, 422e6)
+    z = gpu_compress(dc, x, r, fs, fc, tec)
+    if n <= (1 << 17):
+        ref = np.stack([O.compress(x[i], fs, fc, tec[i], r) for i in range(2)])
+        assert rel_l2(z, ref).max() < TOL
+    else:  # sampled outputs, computed one by one by the oracle
+        idx = np.sort(np.random.default_rng(5).choice(n, 300, replace=False))
+        ref = np.stack([O.compress(x[i], fs, fc, tec[i], r, idx=idx) for i in range(2)])
+        assert rel_l2(z[:, idx], ref).max() < TOL
+
+
+def test_compress_lfm_echo_c3_sampled(dc):
+    # C3 geometry: a dispersed (Eq. 14), delayed LFM echo compressed against the transmitted LFM;
+    # the compressed peak sits at the echo delay, and sampled outputs around it match the oracle
+    n, fs, T, delay = 1 << 20, 2.048e9, 100e-6, 123457
+    L = int(T * fs)
+    r = synth.lfm(L, fs, 413e6, 18e6, T).astype(np.complex64)
+    echo = np.roll(np.concatenate([r, np.zeros(n - L, np.complex64)]), delay)
+    x = O.iono(echo.astype(np.complex128), fs, 0.0, 1e18, distort=True).astype(np.complex64)[None]
+    z = gpu_compress(dc, x, r, fs, 0.0, [1e18], inplace=True)[0]
+    assert int(np.argmax(np.abs(z))) == delay
+    idx = np.unique(np.concatenate([np.arange(delay - 64, delay + 64), np.random.default_rng(9).choice(n, 200)]))
+    ref = O.compress(x[0], fs, 0.0, 1e18, r, idx=idx)
+    assert rel_l2(z[idx], ref).max() < TOL
+    # matched-filter gain: the peak equals the reference energy (Cauchy-Schwarz bound attained)
+    assert abs(abs(z[delay]) / np.sum(np.abs(r.astype(np.complex128)) ** 2) - 1) < 1e-4
+
+
+def test_compress_errors(dc):
+    import torch
+    p = dc.Plan(1 << 17, 2.048e9, 0.0, taps=8)
+    x = torch.zeros(1, 1 << 17, dtype=torch.complex64, device="cuda")
+    with pytest.raises(dc.DispCorrError) as e:
+        p.compress(x, x, [1e18])          # no reference yet
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
+    with pytest.raises(dc.DispCorrError) as e:
+        p.set_reference(torch.zeros((1 << 17) + 1, dtype=torch.complex64, device="cuda"))   # L > n
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
+    q = dc.Plan(4096, 2.048e9, 0.0, taps=8)   # unsupported size
+    with pytest.raises(dc.DispCorrError) as e:
+        q.set_reference(torch.zeros(16, dtype=torch.complex64, device="cuda"))
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
+    p.set_reference(torch.ones(16, dtype=torch.complex64, device="cuda"))
+    buf = torch.zeros(2 << 17, dtype=torch.complex64, device="cuda")
+    import ctypes
+    arr = (ctypes.c_double * 1)(0.0)
+    st = dc.load().dc_compress(p._h, ctypes.c_void_p(buf.data_ptr()), ctypes.c_void_p(buf.data_ptr() + 4096), 1, arr)
+    assert dc.STATUS[st] == "DC_ERR_ALIASING"      # partial overlap of x and z
+    p.compress(x, x, [1e18])                       # in place is allowed
+    p.sync()
