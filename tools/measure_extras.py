@@ -127,7 +127,7 @@ def iono():
         n = 1 << log2n
         bank = synth.waveform_bank(n, count=16)
         x = torch.from_numpy(bank[np.arange(batch) % 16]).cuda()
-        tec = [1e16 * (p % 200) for p in range(batch)]
+        tec = 1e16 * (np.arange(batch) % 200).astype(np.float64)
         p = dc.Plan(n, FS, 0.0, taps=32, stream=stream)
         xs = x.clone()
         ts = time_calls(lambda: p.iono(xs, tec), stream, 50, warm=5)
@@ -159,9 +159,35 @@ def iono():
     return out
 
 
+def iono_sweep():
+    """Ionospheric stage alone (dc_iono, in place) for n = 2^8 .. 2^24 at batch = 2^27 / n samples:
+    samples/s and fraction of HBM (16 B/sample algorithmic; single-kernel regime n <= 2^13 makes
+    one HBM round trip, the four-step regime three)."""
+    hbm, _ = peaks()
+    stream = torch.cuda.Stream()
+    rows = []
+    for log2n in range(8, 25):
+        n = 1 << log2n
+        batch = max(1, (1 << 27) // n)
+        x = synth.complex_gaussian(n, seed=log2n).astype(np.complex64)
+        xs = torch.from_numpy(x).cuda().expand(batch, n).contiguous()
+        tec = 1e16 * (np.arange(batch) % 200).astype(np.float64)  # numpy: no per-call list conversion
+        p = dc.Plan(n, FS, 0.0, taps=8, stream=stream)
+        ts = time_calls(lambda: p.iono(xs, tec), stream, 20, warm=3)
+        ms = float(np.median(ts))
+        sps = batch * n / (ms / 1e3)
+        inf = p.info()
+        rows.append({"n": n, "batch": batch, "ms": ms, "samples_per_s": sps, "frac_hbm": 16 * sps / (hbm * 1e9),
+                     "hbm_round_trips": 1 if inf["regime"] == 0 else 3})
+        p.close()
+        del xs
+        torch.cuda.empty_cache()
+    return {"iono_sweep": rows, "hbm_gbs": hbm}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", nargs="?", default="all", choices=["latency", "sweep", "iono", "all"])
+    ap.add_argument("what", nargs="?", default="all", choices=["latency", "sweep", "iono", "iono_sweep", "all"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0)}
@@ -171,6 +197,8 @@ def main():
         res["iono"] = iono()
     if a.what in ("sweep", "all"):
         res["sweep"] = sweep()
+    if a.what in ("iono_sweep", "all"):
+        res["iono_sweep"] = iono_sweep()
     s = json.dumps(res, indent=1)
     if a.out:
         open(a.out, "w").write(s + "\n")
