@@ -242,17 +242,44 @@ double orc_sinc(double d) {
   return sin(ORC_PI * d) / (ORC_PI * d);
 }
 
-int orc_doppler(int64_t n, int W, double fs, double fc, double alpha, const double *x,
-                double *y) {
-  if (n < 1 || W < 1 || !(alpha > 0.0)) return -1;
+/* ---------------------------------------------------------------------------
+ * Optional taper of the sinc window ("taper window size, taper"; SURVEY
+ * 8(f) NEXT-3; reading R17): Kaiser window of shape parameter kb >= 0 over the
+ * W-sample window, half-width L = W/2,
+ *   taper(d) = I0(kb sqrt(1 - (d/L)^2)) / I0(kb),   d = t - k in [-L, L),
+ * so h(d) = sinc(d) taper(d).  kb = 0 gives taper = 1 exactly (the rectangular
+ * window of R11).  I0 by its power series sum_j ((z/2)^2)^j / (j!)^2.
+ * ------------------------------------------------------------------------- */
+double orc_bessel_i0(double z) {
+  double q = 0.25 * z * z, term = 1.0, sum = 1.0;
+  for (int j = 1; j < 500; ++j) {
+    term *= q / ((double)j * (double)j);
+    sum += term;
+    if (term < 1e-17 * sum) break;
+  }
+  return sum;
+}
+
+double orc_kaiser(double d, double L, double kb) {
+  if (kb == 0.0) return 1.0;
+  double x = d / L;
+  double r = 1.0 - x * x;
+  if (r < 0.0) r = 0.0;
+  return orc_bessel_i0(kb * sqrt(r)) / orc_bessel_i0(kb);
+}
+
+int orc_doppler_win(int64_t n, int W, double fs, double fc, double alpha, double kb,
+                    const double *x, double *y) {
+  if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0)) return -1;
   double beta = 1.0 / alpha;
+  double L = 0.5 * (double)W;
   for (int64_t m = 0; m < n; ++m) {
     double t = (double)m * beta;
     int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W) + 1;
     double re = 0.0, im = 0.0;
     for (int64_t k = k_lo; k < k_lo + W; ++k) {
       if (k < 0 || k >= n) continue;
-      double h = orc_sinc(t - (double)k);
+      double h = orc_sinc(t - (double)k) * orc_kaiser(t - (double)k, L, kb);
       re += x[2 * k] * h;
       im += x[2 * k + 1] * h;
     }
@@ -265,6 +292,12 @@ int orc_doppler(int64_t n, int W, double fs, double fc, double alpha, const doub
     y[2 * m + 1] = re * s + im * c;
   }
   return 0;
+}
+
+/* rectangular window (reading R11) */
+int orc_doppler(int64_t n, int W, double fs, double fc, double alpha, const double *x,
+                double *y) {
+  return orc_doppler_win(n, W, fs, fc, alpha, 0.0, x, y);
 }
 
 /* Exact (unwindowed) Whittaker-Shannon sum over the whole record, Eq. 16,
@@ -297,9 +330,9 @@ int orc_doppler_exact(int64_t n, double fs, double fc, double alpha, const doubl
  * stage: 1 = iono, 2 = doppler, 3 = correct = doppler(iono(x)) with a binary64
  * intermediate (reading R7: iono first).
  * ------------------------------------------------------------------------- */
-int orc_run_batch(int stage, int64_t n, int64_t batch, double fs, double fc, int W,
-                  const double *tec, const double *alpha, const float *x, double *y,
-                  int nthreads, int method) {
+int orc_run_batch_win(int stage, int64_t n, int64_t batch, double fs, double fc, int W, double kb,
+                      const double *tec, const double *alpha, const float *x, double *y,
+                      int nthreads, int method) {
   int err = 0;
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -320,15 +353,21 @@ int orc_run_batch(int stage, int64_t n, int64_t batch, double fs, double fc, int
     if (stage == 1) {
       err |= orc_iono(n, fs, fc, tec[p], method, xin, yp) != 0;
     } else if (stage == 2) {
-      err |= orc_doppler(n, W, fs, fc, alpha[p], xin, yp) != 0;
+      err |= orc_doppler_win(n, W, fs, fc, alpha[p], kb, xin, yp) != 0;
     } else {
       err |= orc_iono(n, fs, fc, tec[p], method, xin, tmp) != 0;
-      err |= orc_doppler(n, W, fs, fc, alpha[p], tmp, yp) != 0;
+      err |= orc_doppler_win(n, W, fs, fc, alpha[p], kb, tmp, yp) != 0;
     }
     free(xin);
     free(tmp);
   }
   return err ? -1 : 0;
+}
+
+int orc_run_batch(int stage, int64_t n, int64_t batch, double fs, double fc, int W,
+                  const double *tec, const double *alpha, const float *x, double *y,
+                  int nthreads, int method) {
+  return orc_run_batch_win(stage, n, batch, fs, fc, W, 0.0, tec, alpha, x, y, nthreads, method);
 }
 
 int orc_max_threads(void) {

@@ -59,6 +59,14 @@ def _load():
         lib.orc_sinc.argtypes = [d]
         lib.orc_doppler.restype = i32
         lib.orc_doppler.argtypes = [i64, i32, d, d, d, p, p]
+        lib.orc_doppler_win.restype = i32
+        lib.orc_doppler_win.argtypes = [i64, i32, d, d, d, d, p, p]
+        lib.orc_bessel_i0.restype = d
+        lib.orc_bessel_i0.argtypes = [d]
+        lib.orc_kaiser.restype = d
+        lib.orc_kaiser.argtypes = [d, d, d]
+        lib.orc_run_batch_win.restype = i32
+        lib.orc_run_batch_win.argtypes = [i32, i64, i64, d, d, i32, d, p, p, p, p, i32, i32]
         lib.orc_doppler_exact.restype = i32
         lib.orc_doppler_exact.argtypes = [i64, d, d, d, p, p]
         lib.orc_run_batch.restype = i32
@@ -143,14 +151,25 @@ def iono(x, fs: float, fc: float, tec: float, direct: bool = False, distort: boo
     return y
 
 
-def doppler(x, W: int, fs: float, fc: float, alpha: float) -> np.ndarray:
-    """Windowed Whittaker-Shannon resampling onto t/alpha, Eq. 16 + window."""
+def doppler(x, W: int, fs: float, fc: float, alpha: float, kaiser: float = 0.0) -> np.ndarray:
+    """Windowed Whittaker-Shannon resampling onto t/alpha, Eq. 16 + window; optional
+    Kaiser taper of shape `kaiser` (reading R17; 0 = rectangular, R11)."""
     x = _c128(x)
     y = np.empty_like(x)
-    rc = _load().orc_doppler(x.size, int(W), fs, fc, alpha, _ptr(x), _ptr(y))
+    rc = _load().orc_doppler_win(x.size, int(W), fs, fc, alpha, float(kaiser), _ptr(x), _ptr(y))
     if rc:
-        raise RuntimeError(f"orc_doppler failed ({rc})")
+        raise RuntimeError(f"orc_doppler_win failed ({rc})")
     return y
+
+
+def bessel_i0(z: float) -> float:
+    """Modified Bessel function I0 by its power series (the taper's definition, R17)."""
+    return _load().orc_bessel_i0(float(z))
+
+
+def kaiser(d: float, L: float, kb: float) -> float:
+    """Kaiser taper I0(kb sqrt(1 - (d/L)^2)) / I0(kb) (R17)."""
+    return _load().orc_kaiser(float(d), float(L), float(kb))
 
 
 def doppler_exact(x, fs: float, fc: float, alpha: float) -> np.ndarray:
@@ -196,7 +215,7 @@ STAGES = {"iono": 1, "doppler": 2, "correct": 3}
 
 
 def run_batch(stage: str, x64: np.ndarray, fs: float, fc: float, W: int,
-              tec=None, alpha=None, nthreads: int = 0, direct: bool = False) -> np.ndarray:
+              tec=None, alpha=None, nthreads: int = 0, direct: bool = False, kaiser: float = 0.0) -> np.ndarray:
     """Batched oracle on complex64 input [batch, n] (upcast exactly), complex128 output."""
     x64 = np.ascontiguousarray(x64, dtype=np.complex64)
     if x64.ndim == 1:
@@ -205,8 +224,8 @@ def run_batch(stage: str, x64: np.ndarray, fs: float, fc: float, W: int,
     tec_a = np.ascontiguousarray(np.zeros(batch) if tec is None else np.broadcast_to(tec, (batch,)), dtype=np.float64)
     alpha_a = np.ascontiguousarray(np.ones(batch) if alpha is None else np.broadcast_to(alpha, (batch,)), dtype=np.float64)
     y = np.empty((batch, n), dtype=np.complex128)
-    rc = _load().orc_run_batch(STAGES[stage], n, batch, fs, fc, int(W), _ptr(tec_a), _ptr(alpha_a),
-                               _ptr(x64), _ptr(y), int(nthreads), 1 if direct else 0)
+    rc = _load().orc_run_batch_win(STAGES[stage], n, batch, fs, fc, int(W), float(kaiser), _ptr(tec_a),
+                                   _ptr(alpha_a), _ptr(x64), _ptr(y), int(nthreads), 1 if direct else 0)
     if rc:
         raise RuntimeError(f"orc_run_batch failed ({rc})")
     return y

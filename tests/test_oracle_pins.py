@@ -423,3 +423,50 @@ def test_compress_lfm_peak_sidelobe_textbook():
     assert -13.8 < sll < -12.8
     wrong = np.abs(np.fft.ifft(np.fft.fft(x) * np.fft.fft(np.pad(r, (0, n - ns)))))
     assert np.max(wrong) < 0.2 * ns
+
+
+# ----------------------------------------------------------------------------- Kaiser taper (R17, NEXT-3)
+def test_bessel_i0_matches_library():
+    # the taper's I0 (power series) against an independent library implementation
+    import scipy.special as sp
+    for z in (0.0, 1e-3, 0.3, 1.0, 3.75, 8.0, 12.5, 20.0):
+        assert abs(O.bessel_i0(z) / sp.i0(z) - 1) < 1e-14, z
+
+
+def test_kaiser_taper_shape():
+    L, kb = 16.0, 8.0
+    assert O.kaiser(0.0, L, kb) == 1.0                                  # centre tap untouched: alpha = 1 stays exact
+    assert O.kaiser(0.0, L, 0.0) == 1.0 and O.kaiser(15.5, L, 0.0) == 1.0   # kb = 0: rectangular (R11)
+    for d in (0.3, 2.5, 7.0, 15.9):
+        assert O.kaiser(d, L, kb) == O.kaiser(-d, L, kb)                 # symmetric
+    assert abs(O.kaiser(L, L, kb) - 1 / 427.56411572180474) < 1e-15     # edge value 1/I0(kb)
+    x = 0.5                                                              # closed form at d = L/2
+    import scipy.special as sp
+    assert abs(O.kaiser(x * L, L, kb) - sp.i0(kb * np.sqrt(1 - x * x)) / sp.i0(kb)) < 1e-14
+
+
+def test_kaiser_alpha_one_identity_and_rect_reduction():
+    x = synth.complex_gaussian(512, seed=3)
+    assert np.array_equal(O.doppler(x, 32, 1e6, 0.0, 1.0, kaiser=8.0), x)         # exact at integer positions
+    a = O.doppler(x, 16, 1e6, 0.0, 1 + 3e-5, kaiser=0.0)
+    b = O.doppler(x, 16, 1e6, 0.0, 1 + 3e-5)
+    assert np.array_equal(a, b)
+
+
+def test_kaiser_taper_accuracy_vs_analytic_truth():
+    # SURVEY 8(c) (independent FP64 scratch code): dilated Tukey LFM at 5 km/s, n = 2^14 (its table used
+    # 2^16), rel-L2 vs the exact undilated chirp.  Rectangular W = 32: 7.3e-3; Kaiser kb = 8:
+    # W = 16: 6.1e-5, W = 32: 3.2e-5.  The taper must reproduce those magnitudes.
+    n, fs = 1 << 14, 2.048e9
+    T = 0.8 * n / fs
+    alpha = O.alpha_from_velocity(5000.0)
+    t = np.arange(n) / fs
+    truth = _tukey_at(t - (n // 10) / fs, T)
+    echo = _tukey_at(alpha * t - (n // 10) / fs, T)
+    nrm = np.linalg.norm(truth)
+    err = lambda W, kb: np.linalg.norm(O.doppler(echo, W, fs, 0.0, alpha, kaiser=kb) - truth) / nrm
+    rect32, k16, k32 = err(32, 0.0), err(16, 8.0), err(32, 8.0)
+    assert 5e-3 < rect32 < 1e-2
+    assert 4e-5 < k16 < 9e-5
+    assert 2e-5 < k32 < 5e-5
+    assert rect32 > 100 * k32

@@ -17,14 +17,17 @@ MUTANTS = {
     "no 1/n": ("for (int64_t t = 0; t < 2 * n; ++t) y[t] /= (double)n;", ""),
     "fft twiddle sign": ("double ang = (double)sign * 2.0 * ORC_PI * (double)j / (double)len;", "double ang = -(double)sign * 2.0 * ORC_PI * (double)j / (double)len;"),
     "window off by one": ("int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W) + 1;", "int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W);"),
-    "resample at alpha": ("double beta = 1.0 / alpha;\n  for (int64_t m = 0; m < n; ++m) {\n    double t = (double)m * beta;\n    int64_t k_lo", "double beta = alpha;\n  for (int64_t m = 0; m < n; ++m) {\n    double t = (double)m * beta;\n    int64_t k_lo"),
-    "carrier sign": ("    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* Exact", "    double ang = 2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* Exact"),
+    "resample at alpha": ("double beta = 1.0 / alpha;\n  double L = 0.5 * (double)W;", "double beta = alpha;\n  double L = 0.5 * (double)W;"),
+    "carrier sign": ("    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* rectangular", "    double ang = 2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* rectangular"),
     "sinc missing pi": ("return sin(ORC_PI * d) / (ORC_PI * d);", "return sin(ORC_PI * d) / (d);"),
     "conj multiply": ("X[2 * k + 1] = xr * s + xi * c;", "X[2 * k + 1] = -xr * s + xi * c;"),
     "drop last sample": ("if (k < 0 || k >= n) continue;", "if (k < 0 || k >= n - 1) continue;"),
     "correlate without conj": ("ar += yr * rr + yi * ri; /* y conj(r) */\n      ai += yi * rr - yr * ri;", "ar += yr * rr - yi * ri;\n      ai += yi * rr + yr * ri;"),
     "correlate lag sign": ("const int64_t t = (s + m) % n;", "const int64_t t = (s - m + n) % n;"),
     "compress skips iono": ("int rc = orc_iono(n, fs, fc, tec, (n & (n - 1)) ? 1 : 0, x, y);", "int rc = 0; memcpy(y, x, sizeof(double) * 2 * (size_t)n);"),
+    "taper half-width W": ("double L = 0.5 * (double)W;", "double L = (double)W;"),
+    "taper not normalised": ("return orc_bessel_i0(kb * sqrt(r)) / orc_bessel_i0(kb);", "return orc_bessel_i0(kb * sqrt(r));"),
+    "I0 series (j!) not squared": ("term *= q / ((double)j * (double)j);", "term *= q / (double)j;"),
     "no u==0 sinc case": ("if (d == 0.0) return 1.0;\n  if (d == floor(d)) return 0.0;", "if (d == 0.0) return 1.0;"),
 }
 
