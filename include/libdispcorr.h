@@ -112,6 +112,14 @@ dc_status dc_compress(dc_plan_t plan, const void *x, void *z, int64_t batch, con
  * alpha[p] == 1 reproduces x[p] bit-exactly. */
 dc_status dc_doppler(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *alpha);
 
+/* Taper of the Doppler stage's sinc window (reading R17; "taper window size, taper"):
+ * Kaiser window of shape `kaiser` over the W = taps window, half-width L = W/2,
+ *   h(d) = sinc(d) I0(kaiser sqrt(1 - (d/L)^2)) / I0(kaiser),  d = t_m - k,
+ * used by dc_doppler and dc_correct from the next call on.  kaiser = 0 (the default) is the
+ * rectangular window of R11.  kaiser must be finite and in [0, 12] (else DC_ERR_INVALID_VALUE).
+ * The centre tap keeps weight 1, so alpha = 1 still reproduces x exactly. */
+dc_status dc_set_taper(dc_plan_t plan, double kaiser);
+
 /* dc_correct = dc_doppler(dc_iono(x)) (iono first, reading R7), x left unchanged,
  * result in y (must not overlap x).  The iono result is kept in a plan-owned,
  * L2-sized chunk buffer between the stages. */

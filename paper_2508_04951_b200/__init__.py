@@ -77,6 +77,7 @@ def load():
         "dc_iono_distort": ([p, p, i64, pd], i32),
         "dc_doppler": ([p, p, p, i64, pd], i32),
         "dc_set_reference": ([p, p, i64], i32),
+        "dc_set_taper": ([p, d], i32),
         "dc_compress": ([p, p, p, i64, pd], i32),
         "dc_correct": ([p, p, p, i64, pd, pd], i32),
         "dc_correct_host": ([p, p, p, i64, pd, pd], i32),
@@ -219,6 +220,11 @@ class Plan:
         tec_a, pt = _f64(tec, batch, "tec")
         _check(load().dc_iono_distort(self._h, px, batch, pt))
         return x
+
+    def set_taper(self, kaiser: float = 0.0):
+        """Kaiser taper (shape `kaiser`, 0 = rectangular) of the Doppler sinc window (reading R17)."""
+        _check(load().dc_set_taper(self._h, float(kaiser)))
+        return self
 
     def set_reference(self, r):
         """Matched-filter reference r (complex64 CUDA tensor of L <= n samples) for compress()."""

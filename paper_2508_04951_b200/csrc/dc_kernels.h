@@ -70,6 +70,15 @@ int tw1024_offset();
 // (var 3 runs passes A and B only)
 cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, int var);
 
+// Kaiser taper of the sinc window (reading R17): K(d) = P(q), q = kb^2/4 (1 - (d/L)^2), L = W/2,
+// P(q) = sum_j q^j / ((j!)^2 I0(kb)) -- the I0 power series, normalised, truncated at kTaperTerms
+constexpr int kTaperTerms = 25;
+struct TaperCoef {
+  float c[kTaperTerms];  // c[j] = 1 / ((j!)^2 I0(kb)), FP32 (from binary64)
+  float qa;              // kb^2 / 4
+  float inv_L2;          // 1 / L^2
+};
+
 struct DopplerArgs {
   const float2 *x;
   float2 *y;
@@ -81,9 +90,11 @@ struct DopplerArgs {
   double carrier_cycles_per_sample;  // fc / fs; carrier phase psi_m = fc (1 - beta) m / fs
   cudaStream_t stream;
   int grid_cap;  // max CTAs of the persistent grid (0: one wave of the whole GPU)
+  bool taper;    // Kaiser taper on (coefficients in tc)
+  TaperCoef tc;
 };
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
-int doppler_path(double max_abs_beta_m1);
+int doppler_path(double max_abs_beta_m1, bool taper = false);
 
 // one persistent kernel for dc_correct of 2^20-sample pulses (fused_correct.cu)
 struct FusedLaunch {

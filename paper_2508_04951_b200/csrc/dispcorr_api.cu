@@ -71,6 +71,9 @@ struct dc_plan_s {
   const float2 *tw1024 = nullptr;  // radix-32 x 32 pass-2 table inside one of the tables above
   float2 *gtab = nullptr;          // per-bin 1/f_k as FP32 pairs, in the layout the warp row kernel reads
   float2 *ref = nullptr;           // conj(R_k) of the matched-filter reference (dc_set_reference), gtab layout
+  bool taper = false;              // Kaiser taper of the sinc window (dc_set_taper, reading R17)
+  double kaiser = 0.0;
+  dc::TaperCoef tc{};
   bool ref_set = false;
   float2 *scratch = nullptr;  // chunk * n samples
   float2 *scratch2 = nullptr;  // second chunk buffer (two chunks in flight on the internal streams)
@@ -322,7 +325,7 @@ dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
                       int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
   int cap = ln.cap;
   if (const char *env = getenv("DISPCORR_DOP_CAP")) cap = atoi(env);  // tuning experiments only
-  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, cap};
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, cap, p->taper, p->tc};
   ProfScope ps(p, DC_K_DOPPLER, pulses * p->n, ln.st);
   DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
   return DC_OK;
@@ -619,6 +622,30 @@ dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
   return DC_OK;
 }
 
+dc_status dc_set_taper(dc_plan_t p, double kaiser) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  if (!std::isfinite(kaiser) || kaiser < 0.0 || kaiser > 12.0)
+    return fail(DC_ERR_INVALID_VALUE, "kaiser = %g must be finite and in [0, 12]", kaiser);
+  // I0(kb) and the normalised series coefficients 1 / ((j!)^2 I0(kb)) in binary64
+  double i0 = 0.0, term = 1.0;
+  const double q = 0.25 * kaiser * kaiser;
+  for (int j = 0; j < 200; ++j) {
+    if (j > 0) term *= q / ((double)j * (double)j);
+    i0 += term;
+    if (term < 1e-18 * i0) break;
+  }
+  double cj = 1.0;
+  for (int j = 0; j < dc::kTaperTerms; ++j) {
+    if (j > 0) cj /= (double)j * (double)j;
+    p->tc.c[j] = (float)(cj / i0);
+  }
+  p->tc.qa = (float)q;
+  p->tc.inv_L2 = (float)(4.0 / ((double)p->taps * (double)p->taps));
+  p->kaiser = kaiser;
+  p->taper = kaiser > 0.0;
+  return DC_OK;
+}
+
 dc_status dc_compress(dc_plan_t p, const void *x, void *z, int64_t batch, const double *tec) {
   return iono_common(p, x, z, batch, tec, 2);
 }
@@ -662,7 +689,7 @@ dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   if ((s = stage_params(p, batch, tec, alpha, &pp, &slot, &mb)) != DC_OK) return s;
   const float2 *xp = (const float2 *)x;
   float2 *yp = (float2 *)y;
-  if (p->fused && p->log2n == 20 && p->regime == 1 && p->tw1024 && p->gtab && dc::doppler_path(mb) != 0) {
+  if (p->fused && !p->taper && p->log2n == 20 && p->regime == 1 && p->tw1024 && p->gtab && dc::doppler_path(mb) != 0) {
     // one persistent kernel: groups of fpg pulses through an L2-sized ring (fused_correct.cu)
     const int64_t ngroups = (batch + p->fpg - 1) / p->fpg;
     if (!p->fring) {

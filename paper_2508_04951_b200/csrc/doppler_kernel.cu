@@ -38,11 +38,11 @@ namespace dc {
 #ifndef DC_DOP_MINB
 #define DC_DOP_MINB 2
 #endif
-template <bool SECOND, int WT>
+template <bool SECOND, int WT, bool TAPER>
 __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
-                        int buf_elems) {
+                        int buf_elems, const __grid_constant__ TaperCoef tc) {
   extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);
   float2 *ob = xs + 2 * buf_elems;  // output staging for coalesced stores
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     phase[bsel] ^= 1u;
     const float2 *sb = xs + bsel * buf_elems;
 
-    dop_tile_compute<SECOND, WT>(sb, cur, W, ob, y, n, carrier);
+    dop_tile_compute<SECOND, WT, 0, TAPER>(sb, cur, W, ob, y, n, carrier, &tc);
     __syncthreads();  // output staging and input buffer bsel free for reuse
     cur = nxt;
     bsel ^= 1;
@@ -86,9 +86,11 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
 // Exact-tap, one-output-per-thread path (Alg. 1 structure) for any alpha.
 // Used when |beta - 1| is too large for the union-window / Taylor scheme, and for alpha == 1
 // pulses handled by the generic path it returns x exactly (u == 0 case).
+template <bool TAPER>
 __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__restrict__ x, float2 *__restrict__ y,
                                                            int64_t n, int W, const PulseParams *__restrict__ pp,
-                                                           int64_t pulse_base, double carrier) {
+                                                           int64_t pulse_base, double carrier,
+                                                           const __grid_constant__ TaperCoef tcoef) {
   const int64_t pulse = blockIdx.y;
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
@@ -112,7 +114,12 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
       const int mm = (int)(k - (int64_t)tc);  // d = t - k = u - mm
       const float d = u - (float)mm;
       const float s = (mm & 1) ? -S : S;
-      const float h = s / d;
+      float h = s / d;
+      if constexpr (TAPER) {
+        float Kt, dKt;
+        kaiser_taper(tcoef, d, Kt, dKt);
+        h *= Kt;
+      }
       const float2 xv = __ldg(xp + k);
       acc.x = fmaf(xv.x, h, acc.x);
       acc.y = fmaf(xv.y, h, acc.y);
@@ -126,7 +133,7 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
   y[pulse * n + m] = acc;
 }
 
-template <bool SECOND, int WT>
+template <bool SECOND, int WT, bool TAPER = false>
 static cudaError_t launch_pipe(const DopplerArgs &a) {
   const int64_t tiles = (a.n + kDopM - 1) / kDopM * a.pulses;
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
@@ -140,7 +147,7 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
     const uint32_t box[2] = {(uint32_t)kDopBox, 1u};
     if (!encode_tile_map(&xmap, a.x, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
   }
-  auto kern = doppler_pipe_kernel<SECOND, WT>;
+  auto kern = doppler_pipe_kernel<SECOND, WT, TAPER>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 2;
@@ -150,30 +157,36 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
   kern<<<(unsigned)grid, kDopT, smem, a.stream>>>(xmap, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample,
-                                                  a.pulses, buf);
+                                                  a.pulses, buf, a.tc);
   return cudaGetLastError();
 }
 
-template <bool SECOND>
+template <bool SECOND, bool TAPER = false>
 static cudaError_t launch_pipe_w(const DopplerArgs &a) {
   switch (a.taps) {  // compile-time tap counts of the benchmark / sweep configurations
-    case 8: return launch_pipe<SECOND, 8>(a);
-    case 16: return launch_pipe<SECOND, 16>(a);
-    case 25: return launch_pipe<SECOND, 25>(a);
-    case 32: return launch_pipe<SECOND, 32>(a);
-    case 64: return launch_pipe<SECOND, 64>(a);
-    case 128: return launch_pipe<SECOND, 128>(a);
-    default: return launch_pipe<SECOND, 0>(a);
+    case 8: return launch_pipe<SECOND, 8, TAPER>(a);
+    case 16: return launch_pipe<SECOND, 16, TAPER>(a);
+    case 25: return launch_pipe<SECOND, 25, TAPER>(a);
+    case 32: return launch_pipe<SECOND, 32, TAPER>(a);
+    case 64: return launch_pipe<SECOND, 64, TAPER>(a);
+    case 128: return launch_pipe<SECOND, 128, TAPER>(a);
+    default: return launch_pipe<SECOND, 0, TAPER>(a);
   }
 }
 
 static cudaError_t launch_doppler_fast(const DopplerArgs &a, bool second) {
+  if (a.taper) return second ? cudaErrorInvalidValue : launch_pipe_w<false, true>(a);
   return second ? launch_pipe_w<true>(a) : launch_pipe_w<false>(a);
 }
 
 static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
   dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)a.pulses);
-  doppler_exact_kernel<<<grid, 256, 0, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample);
+  if (a.taper)
+    doppler_exact_kernel<true><<<grid, 256, 0, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
+                                                          a.carrier_cycles_per_sample, a.tc);
+  else
+    doppler_exact_kernel<false><<<grid, 256, 0, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
+                                                           a.carrier_cycles_per_sample, a.tc);
   return cudaGetLastError();
 }
 
@@ -182,15 +195,17 @@ static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
 //   first order  if drift <= 2e-4 (truncation <= 1.64 delta^2 <= 7e-8 per tap weight)
 //   second order if drift <= 2e-3 (truncation <= 1.3 delta^3 <= 1.1e-8)
 //   exact taps otherwise.
-int doppler_path(double max_abs_beta_m1) {
+// The tapered weights have the first-order path only (h'' of sinc K is not formed): second-order
+// drifts take the exact path.
+int doppler_path(double max_abs_beta_m1, bool taper) {
   const double drift = max_abs_beta_m1 * (kDopR / 2 + 0.5);
   if (drift <= 2.0e-4) return 1;
-  if (drift <= kDopMaxDrift) return 2;
+  if (drift <= kDopMaxDrift && !taper) return 2;
   return 0;
 }
 
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1) {
-  const int path = doppler_path(max_abs_beta_m1);
+  const int path = doppler_path(max_abs_beta_m1, a.taper);
   if (path == 0) return launch_doppler_exact(a);
   return launch_doppler_fast(a, path == 2);
 }

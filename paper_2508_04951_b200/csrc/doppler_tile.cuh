@@ -79,15 +79,31 @@ __device__ __forceinline__ void tap_w(float u, int m, float S, float Cc, float &
   w2 = SECOND ? fmaf(-9.8696044010893586f, w, -2.f * w1 * inv) : 0.f;
 }
 
+// Kaiser taper K(d) and K'(d) (reading R17) by Horner on the normalised I0 series in
+// q = qa (1 - d^2 / L^2); the coefficients sit in the kernel-parameter (constant) bank.
+__device__ __forceinline__ void kaiser_taper(const TaperCoef &tc, float d, float &K, float &dK) {
+  const float q = tc.qa * fmaf(-d * d, tc.inv_L2, 1.0f);
+  float b = tc.c[kTaperTerms - 1], db = 0.f;
+#pragma unroll
+  for (int j = kTaperTerms - 2; j >= 0; --j) {
+    db = fmaf(db, q, b);
+    b = fmaf(b, q, tc.c[j]);
+  }
+  K = b;
+  dK = db * (-2.0f * tc.qa * tc.inv_L2 * d);  // dP/dq * dq/dd
+}
+
 // One doppler tile: R = 9 outputs per thread from the staged span sb (x[Bcta + i] = sb[i]),
 // carrier rotation, then a coalesced store of the tile's M outputs through `ob` (one barrier
 // inside; callers add the trailing barrier before ob / sb are reused).
 // BAR = 0: the whole CTA (kDopT threads) computes the tile; BAR > 0: named barrier BAR over the
 // kDopT threads 0 .. kDopT-1 (the consumer warps of a warp-specialised kernel).
-template <bool SECOND, int WT, int BAR = 0>
+// TAPER: Kaiser-tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only).
+template <bool SECOND, int WT, int BAR = 0, bool TAPER = false>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
-                                                 double carrier) {
+                                                 double carrier, const TaperCoef *tcp = nullptr) {
+  static_assert(!(TAPER && SECOND), "the tapered path is first order");
   const int W = (WT > 0) ? WT : W_rt;
   const double halfW = 0.5 * (double)W;
   const int tid = threadIdx.x;
@@ -180,6 +196,12 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       w = wc;
       w1 = w1c;
       w2 = w2c;
+    }
+    if constexpr (TAPER) {
+      float K, dK;
+      kaiser_taper(*tcp, d, K, dK);
+      w1 = fmaf(w1, K, w * dK);
+      w *= K;
     }
   };
   auto taps = [&](auto TINYc) {

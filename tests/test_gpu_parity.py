@@ -372,3 +372,76 @@ def test_compress_errors(dc):
     assert dc.STATUS[st] == "DC_ERR_ALIASING"      # partial overlap of x and z
     p.compress(x, x, [1e18])                       # in place is allowed
     p.sync()
+
+
+# ----------------------------------------------------------------------------- Kaiser taper (R17, NEXT-3)
+def gpu_doppler_taper(dc, x, W, fs, fc, alpha, kaiser):
+    import torch
+    p = dc.Plan(x.shape[-1], fs, fc, taps=W)
+    p.set_taper(kaiser)
+    t = to_dev(x)
+    y = torch.empty_like(t)
+    p.doppler(t, y, alpha)
+    return from_dev(y)
+
+
+@pytest.mark.parametrize("case", ["fast1", "exact"])
+@pytest.mark.parametrize("W,kb", [(8, 4.0), (16, 8.0), (25, 6.0), (32, 8.0), (64, 10.0), (128, 12.0)])
+def test_doppler_kaiser_vs_oracle(dc, case, W, kb):
+    n = 4096
+    alphas = np.array(ALPHA_CASES[case])
+    x = synth.complex_gaussian(n, seed=W + 7, batch=len(alphas)).astype(np.complex64)
+    for fs, fc in ((2.048e9, 0.0), (51.2e6, 422e6)):
+        y = gpu_doppler_taper(dc, x, W, fs, fc, alphas, kb)
+        ref = O.run_batch("doppler", x, fs, fc, W, None, alphas, kaiser=kb)
+        err = rel_l2(y, ref)
+        assert err.max() < TOL, (case, W, kb, fs, fc, err.max())
+
+
+def test_doppler_kaiser_second_order_drift_takes_exact_path(dc):
+    # |beta - 1| beyond the first-order range: the tapered weights run on the exact-tap path
+    alphas = np.array(ALPHA_CASES["fast2"])
+    x = synth.complex_gaussian(4096, seed=77, batch=3).astype(np.complex64)
+    y = gpu_doppler_taper(dc, x, 32, 2.048e9, 0.0, alphas, 8.0)
+    ref = O.run_batch("doppler", x, 2.048e9, 0.0, 32, None, alphas, kaiser=8.0)
+    assert rel_l2(y, ref).max() < TOL
+
+
+def test_doppler_kaiser_alpha_one_bit_exact_and_accuracy(dc):
+    x = synth.complex_gaussian(8192, seed=3, batch=2).astype(np.complex64)
+    assert np.array_equal(gpu_doppler_taper(dc, x, 32, 51.2e6, 422e6, [1.0, 1.0], 8.0), x)
+    # the GPU path reproduces the taper's accuracy gain against the analytic dilated LFM (R17)
+    from test_oracle_pins import _tukey_at
+    n, fs = 1 << 14, 2.048e9
+    T = 0.8 * n / fs
+    alpha = O.alpha_from_velocity(5000.0)
+    t = np.arange(n) / fs
+    truth = _tukey_at(t - (n // 10) / fs, T)
+    echo = _tukey_at(alpha * t - (n // 10) / fs, T).astype(np.complex64)[None]
+    yk = gpu_doppler_taper(dc, echo, 32, fs, 0.0, [alpha], 8.0)[0]
+    yr = gpu_doppler(dc, echo, 32, fs, 0.0, [alpha])[0]
+    nrm = np.linalg.norm(truth)
+    assert np.linalg.norm(yk - truth) / nrm < 5e-5 < 5e-3 < np.linalg.norm(yr - truth) / nrm
+
+
+def test_correct_kaiser_train_sampled(dc):
+    import torch
+    n, batch = 1 << 16, 6
+    bank = synth.waveform_bank(n, count=3)
+    x = bank[np.arange(batch) % 3]
+    tec, alpha = synth.pulse_params(batch)
+    p = dc.Plan(n, 2.048e9, 0.0, taps=32)
+    p.set_taper(8.0)
+    xd = to_dev(x)
+    yd = torch.empty_like(xd)
+    p.correct(xd, yd, tec, alpha)
+    y = from_dev(yd)
+    idx = [0, 4, 5]
+    ref = O.run_batch("correct", x[idx], 2.048e9, 0.0, 32, tec[idx], alpha[idx], kaiser=8.0)
+    assert rel_l2(y[idx], ref).max() < TOL
+    with pytest.raises(dc.DispCorrError) as e:
+        p.set_taper(-1.0)
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
+    with pytest.raises(dc.DispCorrError) as e:
+        p.set_taper(float("nan"))
+    assert e.value.name == "DC_ERR_INVALID_VALUE"
