@@ -11,7 +11,7 @@ namespace dc {
 
 constexpr int kDopT = 256;  // threads per CTA
 #ifndef DC_DOP_R
-#define DC_DOP_R 9
+#define DC_DOP_R 11
 #endif
 constexpr int kDopR = DC_DOP_R;  // outputs per thread: odd, so lanes' windows (R samples apart) hit distinct banks
 constexpr int kDopM = kDopT * kDopR;     // outputs per tile
