@@ -102,12 +102,14 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
   const uint32_t box[3] = {(uint32_t)kWW, 256, 1};
   if (!encode_tile_map(&smap, a.src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
 #ifndef DC_COL_V1
-  const size_t smem2 = warp_col2_smem_bytes();
+  const size_t smem2 = warp_col3_smem_bytes();
   (void)smem;
-  auto kern = inv ? warp_col2_kernel<true> : warp_col2_kernel<false>;
+  auto kern = inv ? warp_col3_kernel<true> : warp_col3_kernel<false>;
+  constexpr int threads = 2 * kWW * 32;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
 #else
   auto kern = inv ? warp_col_kernel<true> : warp_col_kernel<false>;
+  constexpr int threads = kWW * 32;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 #endif
   if (e != cudaSuccess) return e;
@@ -119,10 +121,10 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
 #else
   const size_t launch_smem = smem;
 #endif
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWW * 32, launch_smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, launch_smem);
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  kern<<<(unsigned)grid, kWW * 32, launch_smem, st>>>(a, smap);
+  kern<<<(unsigned)grid, threads, launch_smem, st>>>(a, smap);
   return cudaGetLastError();
 }
 static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr,

@@ -312,54 +312,63 @@ __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a,
   }
 }
 
-// Column pass, default variant: ONE staging slot per CTA, reused in place as the 8 warps' padded
-// exchange space once the tile is in registers (the tile is 64 KiB, the exchange 8 x 1058
-// samples), so a CTA needs ~80 KiB and two CTAs (16 warps) share an SM: one CTA's TMA load and
-// stores overlap the other CTA's FFTs.  (warp_col_kernel above keeps two staging tiles plus
-// separate exchange buffers in one 196 KiB CTA: 8 warps per SM, latency-bound.)
+// Column pass, default variant: one CTA of TWO 8-warp consumer groups per SM and THREE staging
+// slots.  Local tile i of the CTA goes to group i mod 2 and slot i mod 3; a slot holds the 64 KiB
+// [1024][8] tile and is then reused in place as its group's padded exchange space (8 x 1058
+// samples), so the CTA needs 3 x 68 KiB.  When group g finishes tile i (tile stored, group
+// barrier) it issues the TMA load of tile i + 3 into the freed slot, so two tiles are computed
+// while the third streams in.  (warp_col_kernel above: one 8-warp group, two staging tiles plus
+// separate exchange buffers -- 8 warps per SM and the load latency exposed between tiles.)
 constexpr int kColSlot = ((kWW * kWPad * 8 + 1023) / 1024) * 1024 / 8;  // float2 elements
-__host__ __device__ constexpr size_t warp_col2_smem_bytes() {
-  return (size_t)kColSlot * 8 + kWW * 32 * 8 + 512 * 16 + 16 + 1024;
+constexpr int kColSlots = 3;
+__host__ __device__ constexpr size_t warp_col3_smem_bytes() {
+  return (size_t)kColSlots * kColSlot * 8 + 2 * kWW * 32 * 8 + 512 * 16 + kColSlots * 8 + 1024;
 }
 template <bool INV>
-__global__ void __launch_bounds__(kWW * 32, 2) warp_col2_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
+__global__ void __launch_bounds__(2 * kWW * 32, 1) warp_col3_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
   extern __shared__ __align__(1024) float4 smem4[];
-  float2 *sb = reinterpret_cast<float2 *>(smem4);  // [1024][8] swizzled tile, then 8 exchange buffers
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  float2 *wk = sb + warp * kWPad;
-  float2 *Pw = sb + kColSlot + warp * 32;
-  float4 *Tw = reinterpret_cast<float4 *>(sb + kColSlot + kWW * 32);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(Tw + 512);
+  float2 *slots = reinterpret_cast<float2 *>(smem4);
+  const int tid = threadIdx.x, grp = tid >> 8, gtid = tid & 255, warp = gtid >> 5, lane = tid & 31;
+  float2 *Pw = slots + kColSlots * kColSlot + (grp * kWW + warp) * 32;
+  float4 *Tw = reinterpret_cast<float4 *>(slots + kColSlots * kColSlot + 2 * kWW * 32);
+  uint64_t *full = reinterpret_cast<uint64_t *>(Tw + 512);
   const int log2n = a.log2n;
   const int n = 1 << log2n;
   const uint32_t nmask = (uint32_t)n - 1u;
   const int n2 = n >> 10;
   const int64_t tiles_per_pulse = n2 / kWW;
   const int64_t total = a.pulses * tiles_per_pulse;
+  auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
 
-  for (int i = tid; i < 512; i += kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  auto stage = [&](int64_t it) {  // thread 0 only; every generic access to sb is ordered before it
+  for (int i = tid; i < 512; i += 2 * kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
+  auto stage = [&](int64_t i) {  // one thread; every generic access to the slot is ordered before it
+    const int64_t it = tile_of(i);
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
+    float2 *sb = slots + (i % kColSlots) * kColSlot;
+    uint64_t *bar = &full[i % kColSlots];
     fence_proxy_async();
     mbar_arrive_expect_tx(bar, 1024 * 8 * sizeof(float2));
 #pragma unroll
     for (int b = 0; b < 4; ++b) tma_load_3d(sb + b * 256 * 8, &smap, (int)c0, b * 256, (int)p, bar);
   };
-  int64_t it = blockIdx.x;
   if (tid == 0) {
-    mbar_init(bar, 1);
+    for (int s = 0; s < kColSlots; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
-    if (it < total) stage(it);
+    for (int64_t i = 0; i < kColSlots; ++i)
+      if (tile_of(i) < total) stage(i);
   }
   __syncthreads();
-  unsigned phase = 0u;
-  for (; it < total; it += gridDim.x) {
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+  auto group_sync = [grp] { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(kWW * 32) : "memory"); };
+
+  for (int64_t i = grp; tile_of(i) < total; i += 2) {
+    const int64_t it = tile_of(i);
+    float2 *sb = slots + (i % kColSlots) * kColSlot;
+    float2 *wk = sb + warp * kWPad;
+    mbar_wait(&full[i % kColSlots], (unsigned)((i / kColSlots) & 1));
     float2 v[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) v[r] = sb[col_sw(lane + 32 * r, warp)];
-    __syncthreads();  // the whole tile is in registers: the slot becomes exchange space
+    group_sync();  // the whole tile is in the group's registers: the slot becomes exchange space
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
     if constexpr (!INV) {
       wfft1024<false>(v, wk, Tw, lane);
@@ -376,17 +385,17 @@ __global__ void __launch_bounds__(kWW * 32, 2) warp_col2_kernel(const WarpArgs a
     __syncwarp();
 #pragma unroll
     for (int s = 0; s < 32; ++s) wk[wpad(lane + 32 * s)] = v[s];
-    __syncthreads();
+    group_sync();
     float2 *g = a.dst + p * a.pulse_stride + c0;
 #pragma unroll 4
-    for (int i = tid; i < 1024 * 4; i += kWW * 32) {
-      const int row = i >> 2, v4 = i & 3;
+    for (int j = gtid; j < 1024 * 4; j += kWW * 32) {
+      const int row = j >> 2, v4 = j & 3;
       const float2 e0 = sb[(2 * v4) * kWPad + wpad(row)];
       const float2 e1 = sb[(2 * v4 + 1) * kWPad + wpad(row)];
       __stcg(reinterpret_cast<float4 *>(g + (int64_t)row * n2 + 2 * v4), make_float4(e0.x, e0.y, e1.x, e1.y));
     }
-    __syncthreads();  // slot drained: load the next tile into it
-    if (tid == 0 && it + gridDim.x < total) stage(it + gridDim.x);
+    group_sync();  // slot drained: stream tile i + 3 into it
+    if (gtid == 0 && tile_of(i + kColSlots) < total) stage(i + kColSlots);
   }
 }
 
