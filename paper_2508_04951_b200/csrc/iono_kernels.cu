@@ -51,7 +51,7 @@ static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_
 }
 
 // ---- warp-level 1024-point kernels (wfft.cuh)
-constexpr bool kRowStage = (DC_ROW_NW == 8);
+constexpr bool kRowStage = (DC_ROW_NW <= 12);
 static size_t warp_row_smem(int log2n, int H, bool outer) {
   return RowCfg<DC_ROW_NW, kRowStage>::elems(outer, log2n, H) * sizeof(float2);
 }

@@ -76,14 +76,16 @@ enum RowVar { VAR_CORRECT = 0, VAR_DISTORT = 1, VAR_COMPRESS = 2, VAR_REFERENCE 
 
 // MODE_ROWB: four-step pass B on rows k1 of Z (N2 = 1024).  MODE_SMALL: whole pulses of 1024.
 // NW warps per CTA.  STAGE: each warp prefetches its next row into a private shared buffer with
-// cp.async (8 warps x 255 registers); !STAGE: rows are loaded straight into registers and the
-// latency is hidden by NW = 16 warps (128 registers each).
+// cp.async; !STAGE: rows are loaded straight into registers.  Default NW = 12 (168 registers, Z row
+// staged, g row read from L2): +14% over NW = 8 (255 registers, Z and g staged); NW = 16 spills.
 #ifndef DC_ROW_NW
-#define DC_ROW_NW 8
+#define DC_ROW_NW 12
 #endif
 template <int NW, bool STAGE>
 struct RowCfg {
-  static constexpr int STG = STAGE ? 2048 : 0;  // staging per warp (float2): Z row + g row
+  // staging per warp (float2): Z row, plus the g row when it fits (NW <= 8; NW = 12 reads g from L2)
+  static constexpr bool SG = STAGE && NW <= 8;
+  static constexpr int STG = STAGE ? (SG ? 2048 : 1024) : 0;
   static __host__ __device__ constexpr size_t elems(bool outer, int log2n, int H) {
     // (outer twiddles come from twn(), so no outer-twiddle table is staged)
     return (void)outer, (void)log2n, (void)H, (size_t)NW * (STG + kWPad + 32) + 1024;
@@ -93,6 +95,7 @@ struct RowCfg {
 template <int MODE, int VAR, int NW, bool STAGE>
 __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) {
   using CFG = RowCfg<NW, STAGE>;
+  constexpr bool SG = CFG::SG;
   extern __shared__ float4 smem4[];
   float2 *sm = reinterpret_cast<float2 *>(smem4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,15 +135,21 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
   if constexpr (STAGE) {
     if (it < total) stage_z(it);
     cp_async_commit_();
-    if (it < total) stage_g(it);
-    cp_async_commit_();
+    if constexpr (SG) {
+      if (it < total) stage_g(it);
+      cp_async_commit_();
+    }
   }
   __syncthreads();  // tables visible
 
   for (; it < total; it += G) {
     float2 v[32];
     if constexpr (STAGE) {
-      cp_async_wait_1();  // Z row of this item landed (its g row may still be in flight)
+      if constexpr (SG) {
+        cp_async_wait_1();  // Z row of this item landed (its g row may still be in flight)
+      } else {
+        cp_async_wait_all();  // the only group in flight is this item's Z row
+      }
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = stg[lane + 32 * r];
@@ -161,7 +170,7 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
     // nu = nu_coef * g_k with g_k = 1/f_k from the plan table (0 for f_k <= 0, R3), FP32-pair math
     {
       const float inv_n = (MODE == MODE_ROWB) ? 1.0f : 1.0f / (float)n;  // ROWB: 1/n applied in pass A
-      if constexpr (STAGE) {
+      if constexpr (SG) {
         cp_async_wait_1();  // this item's g row landed (the next Z row may still be in flight)
         __syncwarp();
       }
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
         for (int s = 0; s < 32; ++s) a.ref_out[(int64_t)k1 * 1024 + lane + 32 * s] = make_float2(v[s].x * sc, -v[s].y * sc);
       } else {
         const PulseParams pr = a.pp[a.pulse_base + p];
-        const float2 *grow = STAGE ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
+        const float2 *grow = SG ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
         float2 rc[VAR == VAR_COMPRESS ? 32 : 1];
         if constexpr (VAR == VAR_COMPRESS) {
 #pragma unroll
@@ -181,14 +190,15 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
         }
 #pragma unroll
         for (int s = 0; s < 32; ++s) {
-          const float2 g = grow[lane + 32 * s];
+          if (!SG && s % 8 == 0) asm volatile("" ::: "memory");  // table loads in chunks of 8 (registers)
+          const float2 g = SG ? grow[lane + 32 * s] : __ldg(grow + lane + 32 * s);
           const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
           const float2 w = expm2pi((VAR == VAR_DISTORT) ? -rf : rf);
           v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
           if constexpr (VAR == VAR_COMPRESS) v[s] = cmul(v[s], rc[s]);
         }
       }
-      if constexpr (STAGE) {
+      if constexpr (SG) {
         __syncwarp();  // g staging consumed: prefetch the next g row
         if (it + G < total) stage_g(it + G);
         cp_async_commit_();

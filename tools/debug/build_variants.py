@@ -5,6 +5,7 @@ from paper_2508_04951_b200 import build as b
 V = {
     "x2": ["-DDC_X2=1"],
     "row16": ["-DDC_ROW_NW=16"],
+    "row12": ["-DDC_ROW_NW=12"],
     "nox2": ["-DDC_X2=0"],
     "x2_e16": ["-DDC_X2=1", "-DDC_FS_LOGE=4"],
     "minb1": [],
