@@ -185,9 +185,28 @@ def iono_sweep():
     return {"iono_sweep": rows, "hbm_gbs": hbm}
 
 
+def cpu_oracle():
+    """SURVEY 8(d) CPU oracle timing on this box: dc_correct of C4 pulses (2^20, W = 32) in FP64,
+    (i) one thread -- the plain definition -- and (ii) all host cores (OpenMP over pulses)."""
+    import time
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    n = 1 << 20
+    bank = synth.waveform_bank(n, count=16)
+    tec, alpha = synth.pulse_params(32)
+    out = {"cores": os.cpu_count(), "workload": "C4 dc_correct, 2^20-sample pulses, W = 32, FP64 oracle"}
+    for label, threads, pulses in (("1_thread", 1, 2), ("all_cores", os.cpu_count() or 1, 32)):
+        x = bank[np.arange(pulses) % 16]
+        t0 = time.perf_counter()
+        O.run_batch("correct", x, FS, 0.0, 32, tec[:pulses], alpha[:pulses], nthreads=threads)
+        dt = time.perf_counter() - t0
+        out[label] = {"pulses": pulses, "seconds": dt, "samples_per_s": pulses * n / dt}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", nargs="?", default="all", choices=["latency", "sweep", "iono", "iono_sweep", "all"])
+    ap.add_argument("what", nargs="?", default="all", choices=["latency", "sweep", "iono", "iono_sweep", "cpu", "all"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0)}
@@ -199,6 +218,8 @@ def main():
         res["sweep"] = sweep()
     if a.what in ("iono_sweep", "all"):
         res["iono_sweep"] = iono_sweep()
+    if a.what in ("cpu", "all"):
+        res["cpu_oracle"] = cpu_oracle()
     s = json.dumps(res, indent=1)
     if a.out:
         open(a.out, "w").write(s + "\n")
