@@ -15,6 +15,7 @@ Prints ONE JSON line (rank 0).  Metric: complex samples/s (whole job) and real-t
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -294,9 +295,10 @@ def main():
     # measured DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (profiles/r1_traffic.json: DRAM bytes per sample), scaled to this launch size
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    kname = {"fourstep_A": "warp_col_kernel<0>", "fourstep_B": "warp_row_kernel<2", "fourstep_C": "warp_col_kernel<1>",
-             "doppler": "doppler_pipe_kernel<0, 32>", "fused": "fused_correct_kernel<0, 32>"}.get(dom)
+    tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    tfile = tfiles[-1] if tfiles else ""  # the latest round's capture of the kernels as built
+    kname = {"fourstep_A": "warp_col3_kernel<0>", "fourstep_B": "warp_row_kernel<2", "fourstep_C": "warp_col3_kernel<1>",
+             "doppler": "doppler_pipe_kernel<0, 32, 0>", "fused": "fused_correct_kernel<0, 32>"}.get(dom)
     if os.path.exists(tfile) and kname and n == (1 << 20):
         per = json.load(open(tfile))["dram_bytes_per_sample"]
         hit = [v for k, v in per.items() if kname in k]
