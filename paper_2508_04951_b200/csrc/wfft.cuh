@@ -349,10 +349,12 @@ __global__ void __launch_bounds__(2 * kWW * 32, 1) warp_col3_kernel(const WarpAr
   const int64_t tiles_per_pulse = n2 / kWW;
   const int64_t total = a.pulses * tiles_per_pulse;
   auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+  // pass C walks the tiles last-to-first: the last pulses the row pass wrote are still in L2
+  auto tile_id = [&](int64_t i) { return INV ? total - 1 - tile_of(i) : tile_of(i); };
 
   for (int i = tid; i < 512; i += 2 * kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
   auto stage = [&](int64_t i) {  // one thread; every generic access to the slot is ordered before it
-    const int64_t it = tile_of(i);
+    const int64_t it = tile_id(i);
     const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
     float2 *sb = slots + (i % kColSlots) * kColSlot;
     uint64_t *bar = &full[i % kColSlots];
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(2 * kWW * 32, 1) warp_col3_kernel(const WarpAr
   auto group_sync = [grp] { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(kWW * 32) : "memory"); };
 
   for (int64_t i = grp; tile_of(i) < total; i += 2) {
-    const int64_t it = tile_of(i);
+    const int64_t it = tile_id(i);
     float2 *sb = slots + (i % kColSlots) * kColSlot;
     float2 *wk = sb + warp * kWPad;
     mbar_wait(&full[i % kColSlots], (unsigned)((i / kColSlots) & 1));
