@@ -253,22 +253,24 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       acc[r] = cmul(acc[r], expm2pi(__double2float_rn(psi - rint(psi))));
     }
   }
+  // a warp's 32 x R outputs are contiguous (thread t owns outputs [t R, t R + R)): each warp stages
+  // its own segment and stores it with coalesced 16-byte stores -- no CTA barrier (BAR unused)
 #pragma unroll
   for (int r = 0; r < kDopR; ++r) ob[tid * kDopR + r] = acc[r];
-  if constexpr (BAR == 0) {
-    __syncthreads();
-  } else {
-    asm volatile("bar.sync %0, %1;\n" ::"n"(BAR), "n"(kDopT) : "memory");
-  }
+  __syncwarp();
   {
-    float2 *yp = y + cur.pulse * n + cur.m0;
-    const int64_t valid = min((int64_t)kDopM, n - cur.m0);
-    if (valid == kDopM) {
-      const float4 *o4 = reinterpret_cast<const float4 *>(ob);
+    constexpr int kSeg = 32 * kDopR;  // outputs per warp (even: 16-byte aligned segments)
+    const int w = tid >> 5, lane = tid & 31;
+    const int64_t mw = cur.m0 + (int64_t)w * kSeg;
+    float2 *yp = y + cur.pulse * n + mw;
+    const float2 *os = ob + w * kSeg;
+    const int64_t valid = min((int64_t)kSeg, n - mw);
+    if (valid == kSeg) {
+      const float4 *o4 = reinterpret_cast<const float4 *>(os);
       float4 *y4 = reinterpret_cast<float4 *>(yp);
-      for (int i = tid; i < kDopM / 2; i += kDopT) __stcs(y4 + i, o4[i]);
+      for (int i = lane; i < kSeg / 2; i += 32) __stcs(y4 + i, o4[i]);
     } else {
-      for (int i = tid; i < valid; i += kDopT) yp[i] = ob[i];
+      for (int i = lane; i < valid; i += 32) yp[i] = os[i];
     }
   }
 }
