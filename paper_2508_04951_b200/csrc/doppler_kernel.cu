@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
                         int buf_elems, const __grid_constant__ TaperCoef tc) {
+  pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);
   float2 *ob = xs + 2 * buf_elems;  // output staging for coalesced stores
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
                                                            int64_t n, int W, const PulseParams *__restrict__ pp,
                                                            int64_t pulse_base, double carrier,
                                                            const __grid_constant__ TaperCoef tcoef) {
+  pdl_wait();  // programmatic dependent launch; the trigger is implicit at exit
   const int64_t pulse = blockIdx.y;
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
@@ -156,9 +158,8 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDopT, smem);
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
-  kern<<<(unsigned)grid, kDopT, smem, a.stream>>>(xmap, a.y, a.n, a.taps, a.pp, a.pulse_base, a.carrier_cycles_per_sample,
-                                                  a.pulses, buf, a.tc);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kDopT), smem, a.stream, xmap, a.y, a.n, a.taps, a.pp, a.pulse_base,
+                    a.carrier_cycles_per_sample, a.pulses, buf, a.tc);
 }
 
 template <bool SECOND, bool TAPER = false>
@@ -181,13 +182,9 @@ static cudaError_t launch_doppler_fast(const DopplerArgs &a, bool second) {
 
 static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
   dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)a.pulses);
-  if (a.taper)
-    doppler_exact_kernel<true><<<grid, 256, 0, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
-                                                          a.carrier_cycles_per_sample, a.tc);
-  else
-    doppler_exact_kernel<false><<<grid, 256, 0, a.stream>>>(a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
-                                                           a.carrier_cycles_per_sample, a.tc);
-  return cudaGetLastError();
+  auto kern = a.taper ? doppler_exact_kernel<true> : doppler_exact_kernel<false>;
+  return launch_pdl(kern, grid, dim3(256), 0, a.stream, a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
+                    a.carrier_cycles_per_sample, a.tc);
 }
 
 // Path choice from the largest |beta - 1| among the launched pulses (host-known):

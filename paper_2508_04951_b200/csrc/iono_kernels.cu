@@ -46,8 +46,7 @@ static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CFG::T, smem);
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  kern<<<(unsigned)grid, CFG::T, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(CFG::T), smem, st, a);
 }
 
 // ---- warp-level 1024-point kernels (wfft.cuh)
@@ -71,8 +70,7 @@ static cudaError_t launch_persistent(K kern, size_t smem, int64_t total, const W
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  kern<<<(unsigned)grid, nw * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, st, a);
 }
 template <int MODE>
 static cudaError_t launch_warp_row_mode(const WarpArgs &a, int var, size_t smem, int64_t items, cudaStream_t st, int cap) {
@@ -124,8 +122,7 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, launch_smem);
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  kern<<<(unsigned)grid, threads, launch_smem, st>>>(a, smap);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(threads), launch_smem, st, a, smap);
 }
 static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr,
                           const float2 *ref = nullptr, float2 *ref_out = nullptr) {

@@ -71,6 +71,7 @@ struct TileCfg {
 
 template <int P, int LOGE, int NB, bool ROW, int MODE, bool DISTORT>
 __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_fft_kernel(const TileArgs a) {
+  pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
   using TL = typename CFG::TL;
   using PP = typename CFG::PP;

@@ -94,6 +94,7 @@ struct RowCfg {
 
 template <int MODE, int VAR, int NW, bool STAGE>
 __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) {
+  pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   using CFG = RowCfg<NW, STAGE>;
   constexpr bool SG = CFG::SG;
   extern __shared__ float4 smem4[];
@@ -242,6 +243,7 @@ __device__ __forceinline__ int col_sw(int row, int col) {
 // on staging.  Two staging buffers (2 tiles in flight), one transaction mbarrier each.
 template <bool INV>
 __global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
+  pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   extern __shared__ __align__(1024) float4 smem4[];
   float2 *sm = reinterpret_cast<float2 *>(smem4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -336,6 +338,7 @@ __host__ __device__ constexpr size_t warp_col3_smem_bytes() {
 }
 template <bool INV>
 __global__ void __launch_bounds__(2 * kWW * 32, 1) warp_col3_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
+  pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   extern __shared__ __align__(1024) float4 smem4[];
   float2 *slots = reinterpret_cast<float2 *>(smem4);
   const int tid = threadIdx.x, grp = tid >> 8, gtid = tid & 255, warp = gtid >> 5, lane = tid & 31;

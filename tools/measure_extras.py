@@ -86,6 +86,22 @@ def latency():
     x19 = torch.from_numpy(synth.waveform_bank(n19, count=1)[:1]).cuda()
     p19 = dc.Plan(n19, FS, 0.0, taps=32, stream=stream)
     out["paper_iono_n2^19_batch1"] = stats_us(time_calls(lambda: p19.iono(x19, [1e18]), stream, 1000))
+    # the paper's headline path: ionospheric correction during pulse compression
+    # -- here the matched filter is fused into the phase step (dc_compress, reading R16)
+    with torch.cuda.stream(stream):
+        ref = torch.from_numpy(synth.lfm(int(100e-6 * FS), FS, 420e6, 18e6, 100e-6).astype(np.complex64)).cuda()
+    p19.set_reference(ref)
+    z19 = torch.empty_like(x19)
+    out["paper_compress_n2^19_batch1"] = stats_us(time_calls(lambda: p19.compress(x19, z19, [1e18]), stream, 1000))
+    # compression throughput at the C3 batch (64 x 2^20)
+    xb = torch.from_numpy(synth.waveform_bank(n, count=4)[np.arange(64) % 4]).cuda()
+    zb = torch.empty_like(xb)
+    with torch.cuda.stream(stream):
+        refb = torch.from_numpy(synth.lfm(int(100e-6 * FS), FS, 413e6, 18e6, 100e-6).astype(np.complex64)).cuda()
+    p3.set_reference(refb)
+    tecb = 1e16 * (np.arange(64) % 200).astype(np.float64)
+    ms = float(np.median(time_calls(lambda: p3.compress(xb, zb, tecb), stream, 30, warm=3)))
+    out["C3_compress_64x2^20_throughput"] = {"ms": ms, "samples_per_s": 64 * n / (ms / 1e3)}
     p3.close()
     p19.close()
     return out
