@@ -91,7 +91,7 @@ dc_status dc_iono_distort(dc_plan_t plan, void *x, int64_t batch, const double *
  * r: device float2[L], 1 <= L <= n, the transmitted reference r_0 .. r_{L-1}; it is
  * zero-padded to n and its DFT R_k is computed on the device and kept (conjugated) in
  * the plan (8n bytes), replacing any earlier reference.  r may be reused as soon as
- * the plan's stream has passed this call.  Supported for n = 2^10 and n = 2^17 .. 2^21
+ * the plan's stream has passed this call.  Supported for n = 2^10 and n = 2^14 .. 2^21
  * (the warp-level row-FFT regimes); other n return DC_ERR_INVALID_VALUE. */
 dc_status dc_set_reference(dc_plan_t plan, const void *r, int64_t L);
 

@@ -316,7 +316,7 @@ dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses,
   return DC_OK;
 }
 
-// pulse compression (var 2/3) runs on the warp-level row kernel: n = 2^10 or 2^17 .. 2^21
+// pulse compression (var 2/3) runs on the warp-level row kernel: n = 2^10 or 2^14 .. 2^21
 bool compress_supported(const dc_plan_s *p) {
   return p->tw1024 && p->gtab && ((p->regime == 0 && p->log2n == 10) || (p->regime == 1 && p->P2 == 10));
 }
@@ -385,7 +385,7 @@ dc_status iono_common(dc_plan_t p, const void *x, void *z, int64_t batch, const 
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
   if (var == 2) {
     if (!compress_supported(p))
-      return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^17 .. 2^21 (plan n = %lld)", (long long)p->n);
+      return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^14 .. 2^21 (plan n = %lld)", (long long)p->n);
     if (!p->ref_set) return fail(DC_ERR_INVALID_VALUE, "no matched-filter reference: call dc_set_reference first");
   }
   DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
@@ -604,7 +604,7 @@ dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
   dc_status s;
   if (!compress_supported(p))
-    return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^17 .. 2^21 (plan n = %lld)", (long long)p->n);
+    return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^14 .. 2^21 (plan n = %lld)", (long long)p->n);
   if (L < 1 || L > p->n) return fail(DC_ERR_INVALID_VALUE, "reference length L = %lld must be in [1, n = %lld]", (long long)L, (long long)p->n);
   if ((s = check_device_ptr(p, r, "r")) != DC_OK) return s;
   DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");

@@ -13,6 +13,7 @@
 #include "dc_kernels.h"
 #include "tile_fft.cuh"
 #include "wfft.cuh"
+#include "tcol.cuh"
 #include "tma_host.h"
 
 #include <algorithm>
@@ -124,6 +125,27 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   return launch_pdl(kern, dim3((unsigned)grid), dim3(threads), launch_smem, st, a, smap);
 }
+template <int N1>
+static cudaError_t launch_tcol_n(const WarpArgs &a, bool inv, cudaStream_t st, int cap) {
+  auto kern = inv ? thread_col_kernel<N1, true> : thread_col_kernel<N1, false>;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcolT, 0);
+  const int64_t items = a.pulses * (1024 / 32);  // warp items
+  int64_t grid = std::min<int64_t>((items + kTcolT / 32 - 1) / (kTcolT / 32), (int64_t)sms * std::max(per_sm, 1));
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kTcolT), 0, st, a);
+}
+static cudaError_t launch_tcol(const WarpArgs &a, int P1, bool inv, cudaStream_t st, int cap) {
+  switch (P1) {
+    case 4: return launch_tcol_n<16>(a, inv, st, cap);
+    case 5: return launch_tcol_n<32>(a, inv, st, cap);
+    case 6: return launch_tcol_n<64>(a, inv, st, cap);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr,
                           const float2 *ref = nullptr, float2 *ref_out = nullptr) {
   WarpArgs w{};
@@ -245,7 +267,9 @@ bool describe_fourstep_plan(int P, PlanDesc &d) {
 }
 
 void fourstep_split(int log2n, int &P1, int &P2) {
-  if (log2n >= 17 && log2n <= 21) {  // row pass on the warp-level 1024-point FFT
+  // row pass on the warp-level 1024-point FFT; 2^14 .. 2^16: columns of N1 = 16 .. 64 on the
+  // thread-per-column kernel (tcol.cuh)
+  if (log2n >= 14 && log2n <= 21) {
     P2 = 10;
     P1 = log2n - 10;
     return;
@@ -301,7 +325,7 @@ static cudaError_t launch_row(int P2, const TileArgs &a, cudaStream_t st, int ca
 cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) {
   int P1, P2;
   fourstep_split(f.log2n, P1, P2);
-  // compress / reference need the warp-level row pass (N2 = 1024, n = 2^17 .. 2^21)
+  // compress / reference need the warp-level row pass (N2 = 1024, n = 2^14 .. 2^21)
   const bool warp_row = P2 == 10 && f.tw1024 && f.gtab;
   if (var != VAR_CORRECT && var != VAR_DISTORT && !warp_row) return cudaErrorInvalidValue;
   const bool distort = (var == VAR_DISTORT);
@@ -322,6 +346,7 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) 
       a.dst = f.dst;
       a.twf = f.tw1f;
       if (P1 == 10 && f.tw1024) return launch_warp_col(warp_args(a, f.tw1024), false, f.stream, f.grid_cap);
+      if (P1 <= 6) return launch_tcol(warp_args(a, f.tw1024), P1, false, f.stream, f.grid_cap);
       return launch_col<MODE_COLA>(P1, a, f.stream, f.grid_cap);
     case 1:
       a.src = f.dst;
@@ -336,6 +361,7 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) 
       a.dst = f.dst;
       a.twi = f.tw1i;
       if (P1 == 10 && f.tw1024) return launch_warp_col(warp_args(a, f.tw1024), true, f.stream, f.grid_cap);
+      if (P1 <= 6) return launch_tcol(warp_args(a, f.tw1024), P1, true, f.stream, f.grid_cap);
       return launch_col<MODE_COLC>(P1, a, f.stream, f.grid_cap);
     default: return cudaErrorInvalidValue;
   }

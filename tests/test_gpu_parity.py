@@ -314,7 +314,7 @@ def gpu_compress(dc, x, r, fs, fc, tec, inplace=False):
     return from_dev(z)
 
 
-@pytest.mark.parametrize("log2n,L", [(10, 300), (10, 1024), (17, 8192), (18, 1000), (21, 4096)])
+@pytest.mark.parametrize("log2n,L", [(10, 300), (10, 1024), (14, 500), (16, 2000), (17, 8192), (18, 1000), (21, 4096)])
 def test_compress_vs_oracle(dc, log2n, L):
     # z = circular matched filter of iono(x) against r (oracle: the direct-sum definition)
     n = 1 << log2n
