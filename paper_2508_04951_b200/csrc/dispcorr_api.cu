@@ -67,6 +67,7 @@ struct dc_plan_s {
   int64_t chunk = 1;  // pulses per chunk
   // device tables
   float2 *tw_small_f = nullptr, *tw_small_i = nullptr;
+  float2 *tw_w1024 = nullptr;  // regime 0, n = 2^11 .. 2^13: 1024-point tables of the in-CTA four-step
   float2 *tw1f = nullptr, *tw1i = nullptr, *tw2f = nullptr, *tw2i = nullptr, *twh = nullptr, *twl = nullptr;
   const float2 *tw1024 = nullptr;  // radix-32 x 32 pass-2 table inside one of the tables above
   float2 *gtab = nullptr;          // per-bin 1/f_k as FP32 pairs, in the layout the warp row kernel reads
@@ -482,6 +483,16 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     if ((s = upload(&p->tw_small_i, build_pass_tables(d, true))) != DC_OK) return cleanup(s);
     if (p->log2n == 10 && d.npass == 2 && d.log_radix_fwd[0] == 5 && d.log_radix_fwd[1] == 5)
       p->tw1024 = p->tw_small_f + dc::tw1024_offset();
+    if (p->log2n >= 12 && p->log2n <= 13) {  // n = N1 x 1024 on the warp FFT (wsmall.cuh)
+      dc::PlanDesc d10;
+      dc::describe_small_plan(10, d10);
+      if (d10.npass == 2 && d10.log_radix_fwd[0] == 5 && d10.log_radix_fwd[1] == 5) {
+        if ((s = upload(&p->tw_w1024, build_pass_tables(d10, false))) != DC_OK) return cleanup(s);
+        p->tw1024 = p->tw_w1024 + dc::tw1024_offset();
+        p->P1 = p->log2n - 10;
+        p->P2 = 10;
+      }
+    }
   } else {
     dc::fourstep_split(p->log2n, p->P1, p->P2);
     dc::PlanDesc d1, d2;
@@ -516,7 +527,7 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
   // per-bin g_k = 1/f_k (0 where f_k <= 0, reading R3) for the warp-level row kernel, FP32 pairs:
   // regime 0 (n = 1024): natural bin order; four-step with N2 = 1024: row layout [k1][k2] of k = k1 + N1 k2
   if (p->tw1024) {
-    const int P1 = (p->regime == 0) ? 0 : p->P1;
+    const int P1 = (p->regime == 0 && p->log2n == 10) ? 0 : p->P1;
     std::vector<float2> g((size_t)n);
     for (int64_t k1 = 0; k1 < (1ll << P1); ++k1)
       for (int64_t k2 = 0; k2 < 1024; ++k2) {
@@ -553,7 +564,7 @@ dc_status dc_plan_destroy(dc_plan_t p) {
     if (p->ws[i]) cudaStreamSynchronize(p->ws[i]);
   }
   if (p->fsync) cudaFree(p->fsync);
-  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab, p->fring, p->ref,
+  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw_w1024, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab, p->fring, p->ref,
                     p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
   for (float2 *b : bufs)
     if (b) cudaFree(b);
