@@ -90,8 +90,9 @@ struct DopplerArgs {
   double carrier_cycles_per_sample;  // fc / fs; carrier phase psi_m = fc (1 - beta) m / fs
   cudaStream_t stream;
   int grid_cap;  // max CTAs of the persistent grid (0: one wave of the whole GPU)
-  bool taper;    // Kaiser taper on (coefficients in tc)
+  bool taper;       // Kaiser taper on (coefficients in tc)
   TaperCoef tc;
+  int taper_terms;  // series terms needed (17 or kTaperTerms)
 };
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
 int doppler_path(double max_abs_beta_m1, bool taper = false);

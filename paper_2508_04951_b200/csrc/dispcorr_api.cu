@@ -75,6 +75,7 @@ struct dc_plan_s {
   bool taper = false;              // Kaiser taper of the sinc window (dc_set_taper, reading R17)
   double kaiser = 0.0;
   dc::TaperCoef tc{};
+  int taper_terms = dc::kTaperTerms;
   bool ref_set = false;
   float2 *scratch = nullptr;  // chunk * n samples
   float2 *scratch2 = nullptr;  // second chunk buffer (two chunks in flight on the internal streams)
@@ -326,7 +327,7 @@ dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
                       int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
   int cap = ln.cap;
   if (const char *env = getenv("DISPCORR_DOP_CAP")) cap = atoi(env);  // tuning experiments only
-  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, cap, p->taper, p->tc};
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, cap, p->taper, p->tc, p->taper_terms};
   ProfScope ps(p, DC_K_DOPPLER, pulses * p->n, ln.st);
   DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
   return DC_OK;
@@ -650,6 +651,10 @@ dc_status dc_set_taper(dc_plan_t p, double kaiser) {
     if (j > 0) cj /= (double)j * (double)j;
     p->tc.c[j] = (float)(cj / i0);
   }
+  // 17 series terms suffice when the 17th term is below 1e-9 of the sum over the window (kb <= ~8.9)
+  double t17 = 1.0;
+  for (int j = 1; j <= 17; ++j) t17 *= q / ((double)j * (double)j);
+  p->taper_terms = (t17 / i0 < 1e-9) ? 17 : dc::kTaperTerms;
   p->tc.qa = (float)q;
   p->tc.inv_L2 = (float)(4.0 / ((double)p->taps * (double)p->taps));
   p->kaiser = kaiser;

@@ -38,7 +38,7 @@ namespace dc {
 #ifndef DC_DOP_MINB
 #define DC_DOP_MINB 2
 #endif
-template <bool SECOND, int WT, bool TAPER>
+template <bool SECOND, int WT, int TAPER>
 __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
 // Exact-tap, one-output-per-thread path (Alg. 1 structure) for any alpha.
 // Used when |beta - 1| is too large for the union-window / Taylor scheme, and for alpha == 1
 // pulses handled by the generic path it returns x exactly (u == 0 case).
-template <bool TAPER>
+template <int TAPER>
 __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__restrict__ x, float2 *__restrict__ y,
                                                            int64_t n, int W, const PulseParams *__restrict__ pp,
                                                            int64_t pulse_base, double carrier,
@@ -117,9 +117,9 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
       const float d = u - (float)mm;
       const float s = (mm & 1) ? -S : S;
       float h = s / d;
-      if constexpr (TAPER) {
+      if constexpr (TAPER > 0) {
         float Kt, dKt;
-        kaiser_taper(tcoef, d, Kt, dKt);
+        kaiser_taper<TAPER>(tcoef, d, Kt, dKt);
         h *= Kt;
       }
       const float2 xv = __ldg(xp + k);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
   y[pulse * n + m] = acc;
 }
 
-template <bool SECOND, int WT, bool TAPER = false>
+template <bool SECOND, int WT, int TAPER = 0>
 static cudaError_t launch_pipe(const DopplerArgs &a) {
   const int64_t tiles = (a.n + kDopM - 1) / kDopM * a.pulses;
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
@@ -162,7 +162,7 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
                     a.carrier_cycles_per_sample, a.pulses, buf, a.tc);
 }
 
-template <bool SECOND, bool TAPER = false>
+template <bool SECOND, int TAPER = 0>
 static cudaError_t launch_pipe_w(const DopplerArgs &a) {
   switch (a.taps) {  // compile-time tap counts of the benchmark / sweep configurations
     case 8: return launch_pipe<SECOND, 8, TAPER>(a);
@@ -176,13 +176,17 @@ static cudaError_t launch_pipe_w(const DopplerArgs &a) {
 }
 
 static cudaError_t launch_doppler_fast(const DopplerArgs &a, bool second) {
-  if (a.taper) return second ? cudaErrorInvalidValue : launch_pipe_w<false, true>(a);
+  if (a.taper) {
+    if (second) return cudaErrorInvalidValue;
+    return a.taper_terms <= 17 ? launch_pipe_w<false, 17>(a) : launch_pipe_w<false, kTaperTerms>(a);
+  }
   return second ? launch_pipe_w<true>(a) : launch_pipe_w<false>(a);
 }
 
 static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
   dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)a.pulses);
-  auto kern = a.taper ? doppler_exact_kernel<true> : doppler_exact_kernel<false>;
+  auto kern = !a.taper ? doppler_exact_kernel<0>
+                       : (a.taper_terms <= 17 ? doppler_exact_kernel<17> : doppler_exact_kernel<kTaperTerms>);
   return launch_pdl(kern, grid, dim3(256), 0, a.stream, a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
                     a.carrier_cycles_per_sample, a.tc);
 }

@@ -81,11 +81,13 @@ __device__ __forceinline__ void tap_w(float u, int m, float S, float Cc, float &
 
 // Kaiser taper K(d) and K'(d) (reading R17) by Horner on the normalised I0 series in
 // q = qa (1 - d^2 / L^2); the coefficients sit in the kernel-parameter (constant) bank.
+// NT = number of series terms evaluated (17 when the plan's kb <= 8, else kTaperTerms)
+template <int NT = kTaperTerms>
 __device__ __forceinline__ void kaiser_taper(const TaperCoef &tc, float d, float &K, float &dK) {
   const float q = tc.qa * fmaf(-d * d, tc.inv_L2, 1.0f);
-  float b = tc.c[kTaperTerms - 1], db = 0.f;
+  float b = tc.c[NT - 1], db = 0.f;
 #pragma unroll
-  for (int j = kTaperTerms - 2; j >= 0; --j) {
+  for (int j = NT - 2; j >= 0; --j) {
     db = fmaf(db, q, b);
     b = fmaf(b, q, tc.c[j]);
   }
@@ -98,12 +100,13 @@ __device__ __forceinline__ void kaiser_taper(const TaperCoef &tc, float d, float
 // inside; callers add the trailing barrier before ob / sb are reused).
 // BAR = 0: the whole CTA (kDopT threads) computes the tile; BAR > 0: named barrier BAR over the
 // kDopT threads 0 .. kDopT-1 (the consumer warps of a warp-specialised kernel).
-// TAPER: Kaiser-tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only).
-template <bool SECOND, int WT, int BAR = 0, bool TAPER = false>
+// TAPER > 0: Kaiser-tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only), with
+// TAPER series terms.
+template <bool SECOND, int WT, int BAR = 0, int TAPER = 0>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
                                                  double carrier, const TaperCoef *tcp = nullptr) {
-  static_assert(!(TAPER && SECOND), "the tapered path is first order");
+  static_assert(!(TAPER > 0 && SECOND), "the tapered path is first order");
   const int W = (WT > 0) ? WT : W_rt;
   const double halfW = 0.5 * (double)W;
   const int tid = threadIdx.x;
@@ -197,9 +200,9 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       w1 = w1c;
       w2 = w2c;
     }
-    if constexpr (TAPER) {
+    if constexpr (TAPER > 0) {
       float K, dK;
-      kaiser_taper(*tcp, d, K, dK);
+      kaiser_taper<TAPER>(*tcp, d, K, dK);
       w1 = fmaf(w1, K, w * dK);
       w *= K;
     }
