@@ -289,6 +289,11 @@ bool describe_fourstep_plan(int P, PlanDesc &d) {
 }
 
 void fourstep_split(int log2n, int &P1, int &P2) {
+  if (log2n == 22 || log2n == 23) {  // warp column passes (N1 = 1024) + tile row pass (N2 = 2^12, 2^13):
+    P1 = 10;                         // 63 vs 47 GS/s at 2^22 over the tile-only split
+    P2 = log2n - 10;
+    return;
+  }
   // row pass on the warp-level 1024-point FFT; 2^14 .. 2^16: columns of N1 = 16 .. 64 on the
   // thread-per-column kernel (tcol.cuh)
   if (log2n >= 14 && log2n <= 21) {
