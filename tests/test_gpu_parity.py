@@ -81,7 +81,7 @@ def test_iono_fourstep_regime_vs_oracle(dc, log2n):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("log2n", [21, 22, 24])
+@pytest.mark.parametrize("log2n", [21, 22, 23, 24])
 def test_iono_largest_pulses_vs_oracle(dc, log2n):
     n = 1 << log2n
     x = synth.complex_gaussian(n, seed=log2n, batch=1).astype(np.complex64)
