@@ -1,0 +1,3 @@
+for v in r11b1 r15b1 r17b1 r21b1; do
+ echo "$v $(DISPCORR_LIB=paper_2508_04951_b200/lib/variants/libdispcorr_$v.so timeout 120 python tools/debug/variant_bench.py 20 256 2>&1 | tail -1)"
+done > gpurun_out/s45.log 2>&1
