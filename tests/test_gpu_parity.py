@@ -445,3 +445,24 @@ def test_correct_kaiser_train_sampled(dc):
     with pytest.raises(dc.DispCorrError) as e:
         p.set_taper(float("nan"))
     assert e.value.name == "DC_ERR_INVALID_VALUE"
+
+
+def test_correct_c4_bench_workload_sampled(dc):
+    # The bench's exact workload and launch configuration: the full C4 train (1024 x 2^20, W = 32,
+    # 16 launch groups of 64 pulses), built the way bench.py builds it; parity on the SURVEY 8(d)
+    # sample {0, 64, ..., 960} u {1, 511, 1023}, computed one pulse at a time by the oracle.
+    import torch
+    n, pulses = 1 << 20, 1024
+    cfg = synth.pulse_train(pulses, n)
+    bank_d = torch.from_numpy(cfg["bank"]).cuda()
+    x = bank_d[torch.from_numpy(cfg["index"]).cuda()].contiguous()
+    del bank_d
+    y = torch.empty_like(x)
+    p = dc.Plan(n, cfg["fs"], 0.0, taps=cfg["W"])
+    p.correct(x, y, cfg["tec"], cfg["alpha"])
+    p.sync()
+    idx = sorted(set(range(0, pulses, 64)) | {1, 511, 1023})
+    ys = y[torch.tensor(idx, device="cuda")].cpu().numpy()
+    ref = O.run_batch("correct", cfg["bank"][cfg["index"][idx]], cfg["fs"], 0.0, cfg["W"], cfg["tec"][idx],
+                      cfg["alpha"][idx])
+    assert rel_l2(ys, ref).max() < TOL
