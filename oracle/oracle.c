@@ -324,6 +324,93 @@ int orc_doppler_exact(int64_t n, double fs, double fc, double alpha, const doubl
 }
 
 /* ---------------------------------------------------------------------------
+ * FFT P/Q resampling (Table 2): "the Fourier
+ * transform of the signal has terms removed or added followed by an inverse Fourier
+ * transform" -- the sinc filter becomes a box filter; exact for Nyquist-limited signals
+ * when the number of added/removed samples is an even integer.  Reading R18:
+ *   X = DFT_n(x);  Y (length M) takes the bins of X with |signed frequency| < min(n, M)/2,
+ *   the bin at min(n, M)/2 (even min) is split in half when padding (M > n) and the two
+ *   bins at +-n'/2 are folded together when truncating (M < n);
+ *   y_m = (1/n) sum_{k<M} Y_k exp(+i 2 pi k m / M),  m < min(n, M); zero for M <= m < n,
+ * i.e. the band-limited periodic interpolant of x at t = m n / M (scipy.signal.resample's
+ * convention).  Direct transforms of any length (the definitions written out).
+ * ------------------------------------------------------------------------- */
+int orc_pq_resample(int64_t n, int64_t M, const double *x, double *y) {
+  if (n < 1 || M < 1) return -1;
+  double *X = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+  double *Y = (double *)calloc(2 * (size_t)M, sizeof(double));
+  if (!X || !Y) {
+    free(X);
+    free(Y);
+    return -2;
+  }
+  orc_dft(n, x, X, -1);
+  const int64_t Nm = (n < M) ? n : M;
+  const int64_t nyq = Nm / 2 + 1;               /* bins 0 .. nyq-1: DC, positive (and +Nm/2 when even) */
+  for (int64_t k = 0; k < nyq; ++k) {
+    Y[2 * k] = X[2 * k];
+    Y[2 * k + 1] = X[2 * k + 1];
+  }
+  for (int64_t j = 1; j <= Nm - nyq; ++j) {     /* negative frequencies -1 .. -(Nm - nyq) */
+    Y[2 * (M - j)] = X[2 * (n - j)];
+    Y[2 * (M - j) + 1] = X[2 * (n - j) + 1];
+  }
+  if (Nm % 2 == 0) {
+    const int64_t h = Nm / 2;
+    if (M < n) {                                /* truncation: fold X[-h] into Y[+h] */
+      Y[2 * h] += X[2 * (n - h)];
+      Y[2 * h + 1] += X[2 * (n - h) + 1];
+    } else if (M > n) {                         /* padding: split X[+h] over Y[+h] and Y[-h] */
+      Y[2 * h] *= 0.5;
+      Y[2 * h + 1] *= 0.5;
+      Y[2 * (M - h)] = Y[2 * h];
+      Y[2 * (M - h) + 1] = Y[2 * h + 1];
+    }
+  }
+  double *z = (double *)malloc(sizeof(double) * 2 * (size_t)M);
+  if (!z) {
+    free(X);
+    free(Y);
+    return -2;
+  }
+  orc_dft(M, Y, z, +1);
+  for (int64_t m = 0; m < n; ++m) {
+    y[2 * m] = (m < M) ? z[2 * m] / (double)n : 0.0;
+    y[2 * m + 1] = (m < M) ? z[2 * m + 1] / (double)n : 0.0;
+  }
+  free(X);
+  free(Y);
+  free(z);
+  return 0;
+}
+
+/* Doppler correction by FFT P/Q resampling (reading R18): output m samples the input at
+ * t = m n / M with M = n + 2 round((n alpha - n) / 2) (an even number of samples added or
+ * removed, the paper's exact case), then the carrier term of R10 with beta_eff = n / M. */
+int64_t orc_pq_length(int64_t n, double alpha) {
+  return n + 2 * (int64_t)llround(0.5 * ((double)n * alpha - (double)n));
+}
+
+int orc_doppler_pq(int64_t n, double fs, double fc, double alpha, const double *x, double *y) {
+  if (n < 1 || !(alpha > 0.0)) return -1;
+  const int64_t M = orc_pq_length(n, alpha);
+  if (M < 1) return -1;
+  int rc = orc_pq_resample(n, M, x, y);
+  if (rc) return rc;
+  const double beta_eff = (double)n / (double)M;
+  for (int64_t m = 0; m < n; ++m) {
+    double psi = fc * (1.0 - beta_eff) * (double)m / fs;
+    double r = psi - nearbyint(psi);
+    double ang = -2.0 * ORC_PI * r;
+    double c = cos(ang), sn = sin(ang);
+    double re = y[2 * m], im = y[2 * m + 1];
+    y[2 * m] = re * c - im * sn;
+    y[2 * m + 1] = re * sn + im * c;
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
  * Batched entry points on complex64 inputs (the GPU's input type),
  * upcast exactly to binary64; pulses are independent and may be run
  * on several host threads (nthreads <= 0: OpenMP default).  Output binary64.

@@ -67,6 +67,12 @@ def _load():
         lib.orc_kaiser.argtypes = [d, d, d]
         lib.orc_run_batch_win.restype = i32
         lib.orc_run_batch_win.argtypes = [i32, i64, i64, d, d, i32, d, p, p, p, p, i32, i32]
+        lib.orc_pq_resample.restype = i32
+        lib.orc_pq_resample.argtypes = [i64, i64, p, p]
+        lib.orc_pq_length.restype = i64
+        lib.orc_pq_length.argtypes = [i64, d]
+        lib.orc_doppler_pq.restype = i32
+        lib.orc_doppler_pq.argtypes = [i64, d, d, d, p, p]
         lib.orc_doppler_exact.restype = i32
         lib.orc_doppler_exact.argtypes = [i64, d, d, d, p, p]
         lib.orc_run_batch.restype = i32
@@ -170,6 +176,31 @@ def bessel_i0(z: float) -> float:
 def kaiser(d: float, L: float, kb: float) -> float:
     """Kaiser taper I0(kb sqrt(1 - (d/L)^2)) / I0(kb) (R17)."""
     return _load().orc_kaiser(float(d), float(L), float(kb))
+
+
+def pq_resample(x, M: int) -> np.ndarray:
+    """FFT P/Q resampling of x (length n) to M samples (reading R18), first min(n, M) outputs, zero-padded to n."""
+    x = _c128(x)
+    y = np.empty_like(x)
+    rc = _load().orc_pq_resample(x.size, int(M), _ptr(x), _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_pq_resample failed ({rc})")
+    return y
+
+
+def pq_length(n: int, alpha: float) -> int:
+    """M = n + 2 round((n alpha - n) / 2): an even number of samples added or removed (R18)."""
+    return _load().orc_pq_length(int(n), float(alpha))
+
+
+def doppler_pq(x, fs: float, fc: float, alpha: float) -> np.ndarray:
+    """Doppler correction by FFT P/Q resampling onto t n / M (+ carrier term, R10/R18)."""
+    x = _c128(x)
+    y = np.empty_like(x)
+    rc = _load().orc_doppler_pq(x.size, fs, fc, alpha, _ptr(x), _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_doppler_pq failed ({rc})")
+    return y
 
 
 def doppler_exact(x, fs: float, fc: float, alpha: float) -> np.ndarray:

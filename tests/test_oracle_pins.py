@@ -470,3 +470,45 @@ def test_kaiser_taper_accuracy_vs_analytic_truth():
     assert 4e-5 < k16 < 9e-5
     assert 2e-5 < k32 < 5e-5
     assert rect32 > 100 * k32
+
+
+# ----------------------------------------------------------------------------- FFT P/Q resampling (R18, NEXT-4)
+@pytest.mark.parametrize("n,M", [(64, 70), (64, 58), (63, 71), (65, 60), (100, 102), (101, 99), (256, 250)])
+def test_pq_resample_matches_library(n, M):
+    # independent library implementation of the same definition (FFT, box filter, IFFT, Nyquist split/fold)
+    import scipy.signal as ss
+    rng = np.random.default_rng(n * 1000 + M)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y = O.pq_resample(x, M)
+    k = min(n, M)
+    ref = ss.resample(x, M)[:k]
+    assert np.abs(y[:k] - ref).max() < 1e-12 * np.abs(ref).max()
+    assert not np.any(y[k:])                                  # outputs past M are zero (R12)
+
+
+def test_pq_resample_identity_and_length_rule():
+    x = synth.complex_gaussian(128, seed=11)
+    assert np.allclose(O.pq_resample(x, 128), x, rtol=0, atol=1e-13)
+    assert O.pq_length(1 << 19, 1.0) == 1 << 19
+    a5 = O.alpha_from_velocity(5000.0)                      # n (alpha - 1) = 17.49 samples at 2^19
+    assert O.pq_length(1 << 19, a5) == (1 << 19) + 18         # nearest even number of added samples
+    assert O.pq_length(1 << 19, 1 / a5) == (1 << 19) - 18
+
+
+@pytest.mark.parametrize("n,M", [(96, 100), (96, 90), (127, 131)])
+def test_doppler_pq_exact_for_even_index_dilation(n, M):
+    # Closed form ("exact when N - N/alpha is an even integer"): S(t) = sum_j a_j e^{i 2 pi f_j t / M}
+    # (band-limited, period M) received as x_t = S(alpha t) with alpha = M / n; the correction must
+    # return S(m) exactly.  The windowed sinc of Eq. 16 is not exact for the same input.
+    rng = np.random.default_rng(n + M)
+    f = np.array([0, 3, -5, 11, -17, 23])
+    a = rng.standard_normal(f.size) + 1j * rng.standard_normal(f.size)
+    t = np.arange(n)
+    x = (a[None, :] * np.exp(2j * np.pi * np.outer(t, f) / n)).sum(1)        # S(alpha t), alpha = M / n
+    m = np.arange(min(n, M))
+    truth = (a[None, :] * np.exp(2j * np.pi * np.outer(m, f) / M)).sum(1)    # S(m)
+    y = O.doppler_pq(x, 1e6, 0.0, M / n)
+    assert O.pq_length(n, M / n) == M
+    assert np.abs(y[:m.size] - truth).max() < 1e-11 * np.abs(truth).max()
+    ws = O.doppler(x, 32, 1e6, 0.0, M / n)[:m.size]
+    assert np.abs(ws - truth).max() > 1e-6 * np.abs(truth).max()

@@ -28,6 +28,9 @@ MUTANTS = {
     "taper half-width W": ("double L = 0.5 * (double)W;", "double L = (double)W;"),
     "taper not normalised": ("return orc_bessel_i0(kb * sqrt(r)) / orc_bessel_i0(kb);", "return orc_bessel_i0(kb * sqrt(r));"),
     "I0 series (j!) not squared": ("term *= q / ((double)j * (double)j);", "term *= q / (double)j;"),
+    "pq no Nyquist split": ("      Y[2 * h] *= 0.5;\n      Y[2 * h + 1] *= 0.5;\n", ""),
+    "pq scale 1/M": ("y[2 * m] = (m < M) ? z[2 * m] / (double)n : 0.0;", "y[2 * m] = (m < M) ? z[2 * m] / (double)M : 0.0;"),
+    "pq odd length rule": ("return n + 2 * (int64_t)llround(0.5 * ((double)n * alpha - (double)n));", "return n + (int64_t)llround((double)n * alpha - (double)n);"),
     "no u==0 sinc case": ("if (d == 0.0) return 1.0;\n  if (d == floor(d)) return 0.0;", "if (d == 0.0) return 1.0;"),
 }
 
