@@ -466,3 +466,35 @@ def test_correct_c4_bench_workload_sampled(dc):
     ref = O.run_batch("correct", cfg["bank"][cfg["index"][idx]], cfg["fs"], 0.0, cfg["W"], cfg["tec"][idx],
                       cfg["alpha"][idx])
     assert rel_l2(ys, ref).max() < TOL
+
+
+def test_large_batch_device_param_expansion_is_bit_identical(dc):
+    # batches above 4096 pulses stage raw tec / alpha and derive the per-pulse parameters on the
+    # device; the result must equal the host-derived path bit for bit (same binary64 operations)
+    import torch
+    n, batch = 256, 5000
+    x = torch.from_numpy(synth.complex_gaussian(n, seed=21, batch=batch).astype(np.complex64)).cuda()
+    tec, alpha = synth.pulse_params(batch)
+    p = dc.Plan(n, 2.048e9, 0.0, taps=16)
+    y_big = torch.empty_like(x)
+    p.correct(x, y_big, tec, alpha)                              # one call: device expansion
+    y_small = torch.empty_like(x)
+    for lo in range(0, batch, 2500):                             # two calls: host derivation
+        p.correct(x[lo:lo + 2500], y_small[lo:lo + 2500], tec[lo:lo + 2500], alpha[lo:lo + 2500])
+    p.sync()
+    assert torch.equal(y_big, y_small)
+    xi = x.clone()
+    p.iono(xi, tec)                                              # tec only
+    xs = x.clone()
+    for lo in range(0, batch, 2500):
+        p.iono(xs[lo:lo + 2500], tec[lo:lo + 2500])
+    yd = torch.empty_like(x)
+    p.doppler(x, yd, alpha)                                      # alpha only
+    yd2 = torch.empty_like(x)
+    for lo in range(0, batch, 2500):
+        p.doppler(x[lo:lo + 2500], yd2[lo:lo + 2500], alpha[lo:lo + 2500])
+    p.sync()
+    assert torch.equal(xi, xs) and torch.equal(yd, yd2)
+    idx = [0, 4097, 4999]
+    ref = O.run_batch("correct", x[idx].cpu().numpy(), 2.048e9, 0.0, 16, tec[idx], alpha[idx])
+    assert rel_l2(y_big[idx].cpu().numpy(), ref).max() < TOL
