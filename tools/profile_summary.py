@@ -28,7 +28,7 @@ stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_
 traffic = {}
 md = [f"# {tag} ncu --set full summaries (1 B200, --clock-control none)", "",
       f"Capture: `ncu --set full --import-source on --clock-control none -k regex:<kernels> -s 4 -c 4 -o ... "
-      f"python tools/debug/profile_driver.py 20 64 2` (64 pulses x 2^20 per launch group: {spl:,} samples per launch; "
+      f"python tools/debug/profile_driver.py 20 256 2` (256 pulses x 2^20 per launch group: {spl:,} samples per launch; "
       f"algorithmic bytes = 16 B/sample = {16 * spl / 1e6:.1f} MB per launch).", ""]
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
