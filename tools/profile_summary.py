@@ -13,8 +13,8 @@ tag, rep, launches, spl = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr = rows[0]
-M = [("gpu__time_duration.sum", "duration (us)"), ("dram__bytes_read.sum", "DRAM read (MB)"),
-     ("dram__bytes_write.sum", "DRAM write (MB)"),
+M = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM read"),
+     ("dram__bytes_write.sum", "DRAM write"),
      ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
      ("sm__inst_executed.avg.per_cycle_active", "IPC (active)"),
      ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe % active"),
@@ -23,7 +23,7 @@ M = [("gpu__time_duration.sum", "duration (us)"), ("dram__bytes_read.sum", "DRAM
      ("launch__registers_per_thread", "registers/thread"),
      ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
      ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
-     ("lts__t_bytes.sum", "L2 bytes (MB)"), ("smsp__inst_executed.sum", "warp instructions")]
+     ("lts__t_bytes.sum", "L2 bytes"), ("smsp__inst_executed.sum", "warp instructions")]
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("per_issue_active.ratio")]
 traffic = {}
 md = [f"# {tag} ncu --set full summaries (1 B200, --clock-control none)", "",
@@ -36,7 +36,8 @@ for r in rows[2:]:
     md += [f"## `{name}`", "", "| metric | value |", "|---|---|"]
     for k, label in M:
         if k in hdr:
-            md.append(f"| {label} (`{k}`) | {r[hdr.index(k)]} |")
+            unit = rows[1][hdr.index(k)]
+            md.append(f"| {label} (`{k}`) | {r[hdr.index(k)]} {unit} |")
     rd = float(r[hdr.index("dram__bytes_read.sum")]) if "dram__bytes_read.sum" in hdr else 0
     wr = float(r[hdr.index("dram__bytes_write.sum")]) if "dram__bytes_write.sum" in hdr else 0
     unit = r[hdr.index("dram__bytes_read.sum")] and rows[1][hdr.index("dram__bytes_read.sum")]
