@@ -121,8 +121,9 @@ dc_status dc_doppler(dc_plan_t plan, const void *x, void *y, int64_t batch, cons
 dc_status dc_set_taper(dc_plan_t plan, double kaiser);
 
 /* dc_correct = dc_doppler(dc_iono(x)) (iono first, reading R7), x left unchanged,
- * result in y (must not overlap x).  The iono result is kept in a plan-owned,
- * L2-sized chunk buffer between the stages. */
+ * result in y (must not overlap x).  Pulses run in launch groups of <= 2 GiB; the
+ * ionospheric result of a group is kept in a plan-owned device buffer (allocated on the
+ * first call, sized to min(batch, group)) between the stages. */
 dc_status dc_correct(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *tec,
                      const double *alpha);
 

@@ -415,7 +415,7 @@ dc_status join(dc_plan_s *p) {
   return DC_OK;
 }
 
-// chunk buffers for dc_correct: two (for the two internal streams), min(chunk, batch) pulses each
+// launch-group buffer(s) for dc_correct: one, or two for the two-stream schedule; min(chunk, batch) pulses each
 dc_status ensure_scratch(dc_plan_s *p, int64_t batch) {
   const int64_t need = std::min(p->chunk, batch) * p->n * (int64_t)sizeof(float2);
   if (p->scratch_bytes >= need) return DC_OK;
@@ -430,7 +430,7 @@ dc_status ensure_scratch(dc_plan_s *p, int64_t batch) {
   if (cudaMalloc(&p->scratch, (size_t)need) != cudaSuccess ||
       (p->pipeline && cudaMalloc(&p->scratch2, (size_t)need) != cudaSuccess)) {
     cudaGetLastError();
-    return fail(DC_ERR_OUT_OF_MEMORY, "chunk buffers (2 x %lld bytes)", (long long)need);
+    return fail(DC_ERR_OUT_OF_MEMORY, "launch-group buffer(s) of %lld bytes", (long long)need);
   }
   p->scratch_bytes = need;
   return DC_OK;
