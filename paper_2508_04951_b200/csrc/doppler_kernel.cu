@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
   if (m >= n) return;
   const float2 *xp = x + pulse * n;
   const double beta = pp[pulse_base + pulse].beta;
-  const double t = (double)m * beta;
-  const int64_t K = (int64_t)floor(t - 0.5 * (double)W) + 1;
+  const double t = __dmul_rn((double)m, beta);  // fl(m beta), fl(t - W/2): the oracle's roundings (R9, R14)
+  const int64_t K = (int64_t)floor(__dsub_rn(t, 0.5 * (double)W)) + 1;
   float2 acc = make_float2(0.f, 0.f);
   const double tc = rint(t);
   if (t == tc) {

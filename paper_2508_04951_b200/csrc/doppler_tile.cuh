@@ -114,11 +114,13 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   const int64_t mt = cur.m0 + (int64_t)tid * kDopR;
   const double beta = cur.beta;
   const int lo_shift = (beta < 1.0) ? 1 : 0;
-  const int64_t B = (int64_t)floor((double)mt * beta - halfW) + 1 - lo_shift;
+  // window decisions use the oracle's two separately rounded binary64 operations, fl(fl(m beta) - W/2)
+  // (__dmul_rn / __dsub_rn: never contracted into an FMA), so membership matches R9 exactly
+  const int64_t B = (int64_t)floor(__dsub_rn(__dmul_rn((double)mt, beta), halfW)) + 1 - lo_shift;
   float mask0[kDopR], maskW[kDopR];
 #pragma unroll
   for (int r = 0; r < kDopR; ++r) {
-    const int64_t Kr = (int64_t)floor((double)(mt + r) * beta - halfW) + 1;
+    const int64_t Kr = (int64_t)floor(__dsub_rn(__dmul_rn((double)(mt + r), beta), halfW)) + 1;
     const int a = (int)(Kr - r - B);  // 0 or 1: this output's window offset inside the union
     mask0[r] = (a == 0) ? 1.f : 0.f;
     maskW[r] = (a == 1) ? 1.f : 0.f;

@@ -498,3 +498,16 @@ def test_large_batch_device_param_expansion_is_bit_identical(dc):
     idx = [0, 4097, 4999]
     ref = O.run_batch("correct", x[idx].cpu().numpy(), 2.048e9, 0.0, 16, tec[idx], alpha[idx])
     assert rel_l2(y_big[idx].cpu().numpy(), ref).max() < TOL
+
+
+@pytest.mark.parametrize("alpha", [1.25, 0.8, 1.0 + 2.0 ** -20, 1.0 - 2.0 ** -22, 4.0 / 3.0])
+def test_doppler_window_boundaries_match_oracle(dc, alpha):
+    # alphas whose positions m beta land on or next to integers and half-integers, where a fused
+    # multiply-add (one rounding) and the oracle's fl(fl(m beta) - W/2) (two roundings) can disagree
+    # on window membership (R9); every path must take the oracle's decisions
+    n = 4096
+    x = synth.complex_gaussian(n, seed=31, batch=1).astype(np.complex64)
+    for W in (4, 16, 25, 32):
+        y = gpu_doppler(dc, x, W, 2.048e9, 0.0, [alpha])
+        ref = O.run_batch("doppler", x, 2.048e9, 0.0, W, None, [alpha])
+        assert rel_l2(y, ref).max() < TOL, (alpha, W)
