@@ -201,6 +201,37 @@ def iono_sweep():
     return {"iono_sweep": rows, "hbm_gbs": hbm}
 
 
+def c5_accuracy():
+    """C5 accuracy columns: GPU Doppler correction of an analytically dilated Tukey-10 %
+    LFM (abs-RF, f0 = 411 MHz, B = 18 MHz, T = 0.8 n / fs, v = 5 km/s) against the exact undilated
+    chirp, rel-L2 over the record, rectangular and Kaiser-8 windows, n = 2^12 .. 2^24 x W."""
+    stream = torch.cuda.Stream()
+    alpha = dc.alpha_from_velocity(5000.0)
+    rows = []
+    for log2n in (12, 16, 20, 24):
+        n = 1 << log2n
+        T = 0.8 * n / FS
+        off = n // 10
+        truth = synth.tukey_lfm(n, FS, 411e6, 18e6, T, off)
+        echo = synth.tukey_lfm(n, FS, 411e6, 18e6, T, off / alpha, time_scale=alpha).astype(np.complex64)
+        x = torch.from_numpy(echo[None]).cuda()
+        y = torch.empty_like(x)
+        nrm = np.linalg.norm(truth)
+        for W in (8, 16, 25, 32, 64, 128):
+            row = {"n": n, "W": W}
+            for kb in (0.0, 8.0):
+                p = dc.Plan(n, FS, 0.0, taps=W, stream=stream)
+                p.set_taper(kb)
+                p.doppler(x, y, [alpha])
+                p.sync()
+                err = float(np.linalg.norm(y[0].cpu().numpy().astype(np.complex128) - truth) / nrm)
+                row["rel_l2_rect" if kb == 0 else "rel_l2_kaiser8"] = err
+                p.close()
+            row["rel_l2_uncorrected"] = float(np.linalg.norm(echo - truth) / nrm)
+            rows.append(row)
+    return {"c5_accuracy_vs_analytic": rows, "velocity_mps": 5000.0}
+
+
 def cpu_oracle():
     """SURVEY 8(d) CPU oracle timing on this box: dc_correct of C4 pulses (2^20, W = 32) in FP64,
     (i) one thread -- the plain definition -- and (ii) all host cores (OpenMP over pulses)."""
@@ -222,7 +253,8 @@ def cpu_oracle():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", nargs="?", default="all", choices=["latency", "sweep", "iono", "iono_sweep", "cpu", "all"])
+    ap.add_argument("what", nargs="?", default="all",
+                    choices=["latency", "sweep", "iono", "iono_sweep", "cpu", "c5acc", "all"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0)}
@@ -236,6 +268,8 @@ def main():
         res["iono_sweep"] = iono_sweep()
     if a.what in ("cpu", "all"):
         res["cpu_oracle"] = cpu_oracle()
+    if a.what in ("c5acc", "all"):
+        res["c5_accuracy"] = c5_accuracy()
     s = json.dumps(res, indent=1)
     if a.out:
         open(a.out, "w").write(s + "\n")
