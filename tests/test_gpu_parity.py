@@ -511,3 +511,16 @@ def test_doppler_window_boundaries_match_oracle(dc, alpha):
         y = gpu_doppler(dc, x, W, 2.048e9, 0.0, [alpha])
         ref = O.run_batch("doppler", x, 2.048e9, 0.0, W, None, [alpha])
         assert rel_l2(y, ref).max() < TOL, (alpha, W)
+
+
+def test_iono_c3_geometry_cubic_pin_on_gpu(dc):
+    # f0 = 411 MHz, B = 18 MHz, T = 500 us (1,024,000 samples) in a 2^20 window at
+    # 2.048 GHz, 100 TECU: the GPU's Eq. 15 correction vs the CUBIC truth loses ~0.00135 dB (the
+    # uncorrected echo ~1.347 dB), reproducing the survey's FP64 numbers on the GPU output
+    n, fs, tec, T = 1 << 20, 2.048e9, 1e18, 500e-6
+    x = synth.lfm(n, fs, 411e6, 18e6, T, offset=8192).astype(np.complex64)
+    y = gpu_iono(dc, x[None], fs, 0.0, [tec])[0]
+    cub = L.cubic_waveform(411e6, 18e6, T, O.k2_per_tec() * tec, fs)
+    loss = L.matched_filter_loss_db(y, cub)
+    assert loss < 0.01 and loss == pytest.approx(0.00135, abs=5e-4)
+    assert 1.2 < L.matched_filter_loss_db(x, cub) < 1.5
