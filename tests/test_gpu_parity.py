@@ -524,3 +524,24 @@ def test_iono_c3_geometry_cubic_pin_on_gpu(dc):
     loss = L.matched_filter_loss_db(y, cub)
     assert loss < 0.01 and loss == pytest.approx(0.00135, abs=5e-4)
     assert 1.2 < L.matched_filter_loss_db(x, cub) < 1.5
+
+
+def test_correct_c3_physics_dilated_dispersed_echo(dc):
+    # C3 end to end: the echo of a 411 MHz / 500 us LFM from a target at +5 km/s through 100 TECU is
+    # S(alpha t) (analytic dilation) dispersed by Eq. 14; dc_correct (iono then Doppler, W = 32) must
+    # recover the transmitted chirp up to the windowed-sinc error and the order-of-operations residue
+    # (SURVEY Q15), while the uncorrected echo loses > 1 dB
+    import torch
+    n, fs, tec, T, off = 1 << 20, 2.048e9, 1e18, 500e-6, 8192
+    alpha = O.alpha_from_velocity(5000.0)
+    tx = synth.lfm(n, fs, 411e6, 18e6, T, offset=off)
+    dil = synth.lfm(n, fs, 411e6, 18e6, T, offset=off / alpha, time_scale=alpha)        # S(alpha t)
+    echo = O.iono(dil, fs, 0.0, tec, distort=True).astype(np.complex64)                    # Eq. 14
+    p = dc.Plan(n, fs, 0.0, taps=32)
+    xd = to_dev(echo[None])
+    yd = torch.empty_like(xd)
+    p.correct(xd, yd, [tec], [alpha])
+    y = from_dev(yd)[0]
+    loss = L.matched_filter_loss_db(y, tx[off:off + int(T * fs)])
+    unc = L.matched_filter_loss_db(echo, tx[off:off + int(T * fs)])
+    assert loss < 0.05 and unc > 1.0, (loss, unc)
