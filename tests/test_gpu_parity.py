@@ -542,6 +542,9 @@ def test_correct_c3_physics_dilated_dispersed_echo(dc):
     yd = torch.empty_like(xd)
     p.correct(xd, yd, [tec], [alpha])
     y = from_dev(yd)[0]
-    loss = L.matched_filter_loss_db(y, tx[off:off + int(T * fs)])
-    unc = L.matched_filter_loss_db(echo, tx[off:off + int(T * fs)])
-    assert loss < 0.05 and unc > 1.0, (loss, unc)
+    ref = tx[off:off + int(T * fs)]
+    loss = L.matched_filter_loss_db(y, ref)
+    unc = L.matched_filter_loss_db(echo, ref)
+    iono_only = L.matched_filter_loss_db(from_dev(p.iono(xd.clone(), [tec]))[0], ref)
+    # FP64 oracle on the same input: 1.0e-4 dB corrected, 0.093 dB iono-only, 2.15 dB uncorrected
+    assert loss < 1e-3 and iono_only > 0.05 and unc > 2.0, (loss, iono_only, unc)
