@@ -512,3 +512,66 @@ def test_doppler_pq_exact_for_even_index_dilation(n, M):
     assert np.abs(y[:m.size] - truth).max() < 1e-11 * np.abs(truth).max()
     ws = O.doppler(x, 32, 1e6, 0.0, M / n)[:m.size]
     assert np.abs(ws - truth).max() > 1e-6 * np.abs(truth).max()
+
+
+# ----------------------------------------------------------------------------- carrier term at fc != 0 (R10, R18)
+def _baseband_echo_of_dilated_rf(g_hz, amp, fs, fc, alpha, n):
+    """Received baseband samples r_k = S_bb(alpha t) e^{i 2 pi fc (alpha - 1) t}, t = k / fs: the echo
+    S_RF(alpha t) (Eq. 13) of S_RF(t) = S_bb(t) e^{i 2 pi fc t}, mixed down by an LO at fc."""
+    t = np.arange(n) / fs
+    ph = np.outer(alpha * t, g_hz) + (fc * (alpha - 1.0) * t)[:, None]
+    return (amp[None, :] * np.exp(2j * np.pi * (ph - np.floor(ph)))).sum(1)
+
+
+@pytest.mark.parametrize("n,M", [(96, 100), (128, 122)])
+def test_doppler_pq_carrier_recovers_transmitted_baseband(n, M):
+    # Physical truth at fc != 0 (P:L294 exact case; reading R18 + R10): choose baseband tones g_j so the
+    # received echo of S_RF(alpha_eff t), alpha_eff = M / n, is periodic in n and band-limited (every
+    # component on an n-point bin).  P/Q resampling to M then samples the echo exactly at t = m n / M and
+    # the carrier term (beta_eff = n / M, the grid actually resampled) must leave S_bb(m / fs) -- the
+    # transmitted baseband -- for every m < min(n, M).  alpha passed to the method is NOT M / n exactly
+    # (it only selects M), so a carrier computed from 1 / alpha, or with the wrong sign, fails.
+    fs, fc = 51.2e6, 422e6
+    a_eff = M / n
+    f_bins = np.array([0, 2, -3, 7, -9, 13])
+    rng = np.random.default_rng(7 * n + M)
+    amp = rng.standard_normal(f_bins.size) + 1j * rng.standard_normal(f_bins.size)
+    g = (f_bins * fs / n - fc * (a_eff - 1.0)) / a_eff          # a_eff g_j + fc (a_eff - 1) = f_j fs / n
+    x = _baseband_echo_of_dilated_rf(g, amp, fs, fc, a_eff, n)
+    alpha = a_eff * (1.0 + 0.6 / n)                              # rounds to the same M (pq_length)
+    assert O.pq_length(n, alpha) == M
+    m = np.arange(min(n, M))
+    ph = np.outer(m / fs, g)
+    truth = (amp[None, :] * np.exp(2j * np.pi * (ph - np.floor(ph)))).sum(1)   # S_bb(m / fs)
+    y = O.doppler_pq(x, fs, fc, alpha)
+    assert np.abs(y[:m.size] - truth).max() < 1e-9 * np.abs(truth).max()
+    # the same input without the carrier term (fc passed as 0 shifts the bin grid, so compare the pure
+    # resampling instead): the residual carrier exp(i 2 pi fc (1 - n/M) m / fs) is large
+    y0 = O.pq_resample(x, M)[:m.size]
+    assert np.abs(y0 - truth).max() > 0.1 * np.abs(truth).max()
+
+
+def test_doppler_exact_carrier_term_baseband():
+    # Eq. 16 over the whole record (orc_doppler_exact) with the R10 carrier at fc = 422 MHz: the
+    # corrected echo of a dilated baseband LFM (the same physics as test_doppler_carrier_term_baseband)
+    # matches the transmitted pulse; dropping the carrier (or flipping it: twice the residual) costs > 0.1 dB.
+    n, fs, fc, T = 4096, 51.2e6, 422e6, 40e-6
+    alpha = O.alpha_from_velocity(5000.0)
+    t = np.arange(n) / fs
+    off = 48 / fs
+
+    def sbb(tt):
+        tau = tt - off
+        inside = (tau >= 0) & (tau < T)
+        cyc = (413e6 - fc) * tau + 0.5 * 18e6 * tau * tau / T
+        v = np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+        v[~inside] = 0
+        return v
+
+    truth = sbb(t)
+    cyc = fc * (alpha - 1) * t
+    echo = sbb(alpha * t) * np.exp(2j * np.pi * (cyc - np.floor(cyc)))
+    with_c = L.matched_filter_loss_db(O.doppler_exact(echo, fs, fc, alpha), truth)
+    without = L.matched_filter_loss_db(O.doppler_exact(echo, fs, 0.0, alpha), truth)
+    assert with_c < 0.01
+    assert without > 0.1

@@ -32,6 +32,11 @@ MUTANTS = {
     "pq scale 1/M": ("y[2 * m] = (m < M) ? z[2 * m] / (double)n : 0.0;", "y[2 * m] = (m < M) ? z[2 * m] / (double)M : 0.0;"),
     "pq odd length rule": ("return n + 2 * (int64_t)llround(0.5 * ((double)n * alpha - (double)n));", "return n + (int64_t)llround((double)n * alpha - (double)n);"),
     "no u==0 sinc case": ("if (d == 0.0) return 1.0;\n  if (d == floor(d)) return 0.0;", "if (d == 0.0) return 1.0;"),
+    "pq carrier sign": ("    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), sn = sin(ang);", "    double ang = 2.0 * ORC_PI * r;\n    double c = cos(ang), sn = sin(ang);"),
+    "pq carrier from 1/alpha": ("const double beta_eff = (double)n / (double)M;", "const double beta_eff = 1.0 / alpha;"),
+    "pq no carrier": ("double psi = fc * (1.0 - beta_eff) * (double)m / fs;", "double psi = 0.0 * fc * (1.0 - beta_eff) * (double)m / fs;"),
+    "exact carrier sign": ("    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---", "    double ang = 2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---"),
+    "exact no carrier": ("    double psi = fc * (1.0 - beta) * (double)m / fs;\n    double r = psi - nearbyint(psi);\n    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---", "    double psi = 0.0;\n    double r = psi - nearbyint(psi);\n    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---"),
 }
 
 failed_to_catch = []
