@@ -268,20 +268,7 @@ def main():
         return out
 
     kern = profile(plan)
-    # per-stage breakdown with the multi-kernel schedule (same kernels' arithmetic, one launch per
-    # stage per launch group): a separate plan built with DISPCORR_FUSED=0
     stages = None
-    if "fused" in kern:
-        old = os.environ.get("DISPCORR_FUSED")
-        os.environ["DISPCORR_FUSED"] = "0"
-        plan_s = dc.Plan(n, FS, 0.0, taps=taps, stream=stream)
-        if old is None:
-            del os.environ["DISPCORR_FUSED"]
-        else:
-            os.environ["DISPCORR_FUSED"] = old
-        plan_s.correct(x, y, tec_r, alpha_r)
-        stages = profile(plan_s)
-        plan_s.close()
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches"])
     src = stages if stages else kern
     fft_names = [k for k in src if k not in ("doppler", "fused")]
@@ -308,31 +295,6 @@ def main():
                 "frac": kern[dom]["gbs"] / hbm, "traffic": traffic, "kernel": dom, "peak_source": peak_kind,
                 "bytes_per_sample": 16, "algorithmic_bytes_per_launch": 16 * kern[dom]["samples_per_launch"],
                 "kernels": kern, "stages_multi_kernel": stages, "fft_stage": fft_stage}
-
-    # ---------------- the opt-in single persistent kernel (DISPCORR_FUSED=1), timed the same way
-    alternatives = None
-    if n == (1 << 20) and os.environ.get("DISPCORR_FUSED") != "1":
-        old = os.environ.get("DISPCORR_FUSED")
-        os.environ["DISPCORR_FUSED"] = "1"
-        plan_f = dc.Plan(n, FS, 0.0, taps=taps, stream=stream)
-        if old is None:
-            del os.environ["DISPCORR_FUSED"]
-        else:
-            os.environ["DISPCORR_FUSED"] = old
-        for _ in range(2):
-            plan_f.correct(x, y, tec_r, alpha_r)
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            f0.record(stream)
-            for _ in range(args.steps):
-                plan_f.correct(x, y, tec_r, alpha_r)
-            f1.record(stream)
-        f1.synchronize()
-        fms = max_over_ranks(f0.elapsed_time(f1), device="cuda")
-        alternatives = {"fused_single_kernel": {"value": pulses * n * args.steps / (fms / 1e3), "unit": UNIT,
-                                                "note": "opt-in DISPCORR_FUSED=1; not the default (slower)"}}
-        plan_f.close()
-        plan.correct(x, y, tec_r, alpha_r)  # leave y from the default path for the e2e check below
 
     # ---------------- end to end through the public host-buffer API (pinned host memory)
     e2e = None
@@ -380,7 +342,6 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "alternatives": alternatives,
         }
         print(json.dumps(line), flush=True)
     plan.close()

@@ -268,30 +268,54 @@ double orc_kaiser(double d, double L, double kb) {
   return orc_bessel_i0(kb * sqrt(r)) / orc_bessel_i0(kb);
 }
 
+/* one output m of the windowed, optionally tapered Eq. 16 with the R10 carrier (the steps above) */
+static void orc_doppler_one(int64_t n, int W, double fs, double fc, double beta, double kb, const double *x,
+                            int64_t m, double *ym) {
+  double L = 0.5 * (double)W;
+  double t = (double)m * beta;
+  int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W) + 1;
+  double re = 0.0, im = 0.0;
+  for (int64_t k = k_lo; k < k_lo + W; ++k) {
+    if (k < 0 || k >= n) continue;
+    double h = orc_sinc(t - (double)k) * orc_kaiser(t - (double)k, L, kb);
+    re += x[2 * k] * h;
+    im += x[2 * k + 1] * h;
+  }
+  /* carrier rotation; cycles reduced mod 1 (period 1) before the angle */
+  double psi = fc * (1.0 - beta) * (double)m / fs;
+  double r = psi - nearbyint(psi);
+  double ang = -2.0 * ORC_PI * r;
+  double c = cos(ang), s = sin(ang);
+  ym[0] = re * c - im * s;
+  ym[1] = re * s + im * c;
+}
+
 int orc_doppler_win(int64_t n, int W, double fs, double fc, double alpha, double kb,
                     const double *x, double *y) {
   if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0)) return -1;
   double beta = 1.0 / alpha;
-  double L = 0.5 * (double)W;
-  for (int64_t m = 0; m < n; ++m) {
-    double t = (double)m * beta;
-    int64_t k_lo = (int64_t)floor(t - 0.5 * (double)W) + 1;
-    double re = 0.0, im = 0.0;
-    for (int64_t k = k_lo; k < k_lo + W; ++k) {
-      if (k < 0 || k >= n) continue;
-      double h = orc_sinc(t - (double)k) * orc_kaiser(t - (double)k, L, kb);
-      re += x[2 * k] * h;
-      im += x[2 * k + 1] * h;
-    }
-    /* carrier rotation; cycles reduced mod 1 (period 1) before the angle */
-    double psi = fc * (1.0 - beta) * (double)m / fs;
-    double r = psi - nearbyint(psi);
-    double ang = -2.0 * ORC_PI * r;
-    double c = cos(ang), s = sin(ang);
-    y[2 * m] = re * c - im * s;
-    y[2 * m + 1] = re * s + im * c;
-  }
+  for (int64_t m = 0; m < n; ++m) orc_doppler_one(n, W, fs, fc, beta, kb, x, m, y + 2 * m);
   return 0;
+}
+
+/* The same outputs at the nidx sample positions idx[] only (parity at sizes where the whole
+ * pulse would take too long); OpenMP over the samples. */
+int orc_doppler_at(int64_t n, int W, double fs, double fc, double alpha, double kb, const double *x,
+                   int64_t nidx, const int64_t *idx, double *y) {
+  if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0)) return -1;
+  double beta = 1.0 / alpha;
+  int err = 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) reduction(| : err)
+#endif
+  for (int64_t i = 0; i < nidx; ++i) {
+    if (idx[i] < 0 || idx[i] >= n) {
+      err |= 1;
+      continue;
+    }
+    orc_doppler_one(n, W, fs, fc, beta, kb, x, idx[i], y + 2 * i);
+  }
+  return err ? -1 : 0;
 }
 
 /* rectangular window (reading R11) */

@@ -61,6 +61,8 @@ def _load():
         lib.orc_doppler.argtypes = [i64, i32, d, d, d, p, p]
         lib.orc_doppler_win.restype = i32
         lib.orc_doppler_win.argtypes = [i64, i32, d, d, d, d, p, p]
+        lib.orc_doppler_at.restype = i32
+        lib.orc_doppler_at.argtypes = [i64, i32, d, d, d, d, p, i64, p, p]
         lib.orc_bessel_i0.restype = d
         lib.orc_bessel_i0.argtypes = [d]
         lib.orc_kaiser.restype = d
@@ -165,6 +167,18 @@ def doppler(x, W: int, fs: float, fc: float, alpha: float, kaiser: float = 0.0) 
     rc = _load().orc_doppler_win(x.size, int(W), fs, fc, alpha, float(kaiser), _ptr(x), _ptr(y))
     if rc:
         raise RuntimeError(f"orc_doppler_win failed ({rc})")
+    return y
+
+
+def doppler_at(x, W: int, fs: float, fc: float, alpha: float, idx, kaiser: float = 0.0) -> np.ndarray:
+    """The outputs of doppler() at the sample positions idx only (same arithmetic per output)."""
+    x = _c128(x)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    y = np.empty(idx.size, np.complex128)
+    rc = _load().orc_doppler_at(x.size, int(W), fs, fc, alpha, float(kaiser), _ptr(x), idx.size,
+                                idx.ctypes.data_as(ctypes.c_void_p), _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_doppler_at failed ({rc})")
     return y
 
 

@@ -20,11 +20,10 @@ import os
 
 import numpy as np
 
-__all__ = ["Plan", "DispCorrError", "alpha_from_velocity", "k2_per_tec", "library_path", "load", "STATUS"]
+__all__ = ["Plan", "DispCorrError", "alpha_from_velocity", "k2_per_tec", "library_path", "load", "use_library", "STATUS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# DISPCORR_LIB selects an alternative in-tree build (kernel tuning variants, tools/debug/)
-_LIB_PATH = os.environ.get("DISPCORR_LIB", os.path.join(_HERE, "lib", "libdispcorr.so"))
+_LIB_PATH = os.path.join(_HERE, "lib", "libdispcorr.so")
 _lib = None
 
 STATUS = {
@@ -56,6 +55,15 @@ class PlanInfo(ctypes.Structure):
 
 def library_path() -> str:
     return _LIB_PATH
+
+
+def use_library(path: str):
+    """Kernel-tuning tools only: load an alternative in-tree build (e.g. one compiled with extra -D
+    flags by ``build.build(out=...)``) instead of lib/libdispcorr.so.  Must precede the first load()."""
+    global _LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("libdispcorr is already loaded")
+    _LIB_PATH = os.path.abspath(path)
 
 
 def load():
@@ -156,6 +164,7 @@ class Plan:
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
+        explicit_stream = stream is not None
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         self.n, self.fs, self.fc, self.taps = int(n), float(fs), float(fc), int(taps)
@@ -164,6 +173,8 @@ class Plan:
                            ctypes.c_void_p(stream.cuda_stream)))
         self._h = h
         self._stream = stream
+        # an explicit stream pins the plan to it; otherwise calls follow torch's current stream
+        self.follow_current_stream = not explicit_stream
 
     # -- lifecycle
     def close(self):
@@ -184,8 +195,24 @@ class Plan:
         self.close()
 
     def set_stream(self, stream):
+        """Pin the plan to `stream` (it stops following torch's current stream); later work on
+        `stream` is ordered after the plan's earlier work (dc_set_stream)."""
+        self._retarget(stream)
+        self.follow_current_stream = False
+
+    def _retarget(self, stream):
         _check(load().dc_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)))
         self._stream = stream
+
+    def _follow_stream(self):
+        # enqueue on torch's current stream of the plan's device (like a torch op), with the
+        # plan's earlier work ordered before it (dc_set_stream)
+        if not self.follow_current_stream:
+            return
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self._stream.cuda_stream:
+            self._retarget(cur)
 
     def sync(self):
         _check(load().dc_sync(self._h))
@@ -211,6 +238,7 @@ class Plan:
         """Eq. 15 ionospheric correction of x [batch, n] in place; tec in el/m^2 per pulse."""
         px, batch = _dev_ptr(x, "x", self.n)
         tec_a, pt = _f64(tec, batch, "tec")
+        self._follow_stream()
         _check(load().dc_iono(self._h, px, batch, pt))
         return x
 
@@ -218,6 +246,7 @@ class Plan:
         """Eq. 14 forward ionospheric model of x [batch, n] in place."""
         px, batch = _dev_ptr(x, "x", self.n)
         tec_a, pt = _f64(tec, batch, "tec")
+        self._follow_stream()
         _check(load().dc_iono_distort(self._h, px, batch, pt))
         return x
 
@@ -231,6 +260,7 @@ class Plan:
         import torch
         if not isinstance(r, torch.Tensor) or r.dtype != torch.complex64 or not r.is_cuda or not r.is_contiguous():
             raise TypeError("r must be a contiguous complex64 CUDA tensor")
+        self._follow_stream()
         _check(load().dc_set_reference(self._h, ctypes.c_void_p(r.data_ptr()), int(r.numel())))
         self._ref = r  # keep alive until the plan stream has consumed it
         return self
@@ -242,6 +272,7 @@ class Plan:
         if bz != batch:
             raise ValueError("x and z batch sizes differ")
         tec_a, pt = _f64(tec, batch, "tec")
+        self._follow_stream()
         _check(load().dc_compress(self._h, px, pz, batch, pt))
         return z
 
@@ -252,6 +283,7 @@ class Plan:
         if by != batch:
             raise ValueError("x and y batch sizes differ")
         alpha_a, pa = _f64(alpha, batch, "alpha")
+        self._follow_stream()
         _check(load().dc_doppler(self._h, px, py, batch, pa))
         return y
 
@@ -263,6 +295,7 @@ class Plan:
             raise ValueError("x and y batch sizes differ")
         tec_a, pt = _f64(tec, batch, "tec")
         alpha_a, pa = _f64(alpha, batch, "alpha")
+        self._follow_stream()
         _check(load().dc_correct(self._h, px, py, batch, pt, pa))
         return y
 
@@ -274,5 +307,6 @@ class Plan:
             raise ValueError("x and y batch sizes differ")
         tec_a, pt = _f64(tec, batch, "tec")
         alpha_a, pa = _f64(alpha, batch, "alpha")
+        self._follow_stream()
         _check(load().dc_correct_host(self._h, px, py, batch, pt, pa))
         return y_host

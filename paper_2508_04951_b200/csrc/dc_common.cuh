@@ -52,9 +52,10 @@ __host__ __device__ inline double k2_per_tec() { return (kQe * kQe) / (8.0 * kPi
 struct PulseParams {
   double nu_coef;  // 2 K2 / c = 2 * k2_per_tec * tec / c  [cycles * Hz]; nu_k = nu_coef / f_k  (Eq. 14/15)
   double beta;     // 1 / alpha (binary64, computed on the host exactly as the oracle does)
+  double k2;       // K2 = k2_per_tec * tec (Eq. 1), for the exact binary64 phase of huge-|nu| bins
   float nu_hi, nu_lo;  // nu_coef as an unevaluated FP32 pair (hi + lo), for the FP32 phase path
-  float pad0, pad1;
 };
+static_assert(sizeof(PulseParams) == 32, "PulseParams is 32 bytes per pulse");
 
 // Eq. 15 phase cycles nu = nu_coef * g (g = 1/f_k from the plan's per-bin FP32-pair table) reduced
 // mod 1, entirely in FP32 pair arithmetic: p + e = hi*gh exactly (FMA), lo terms in FP32.  Returns
@@ -67,6 +68,30 @@ __device__ __forceinline__ float phase_frac(float hi, float lo, float2 g) {
   const float fr = p - rintf(p);  // exact; 0 when |p| >= 2^23 (p is then an integer)
   const float t = fr + l;
   return t - rintf(t);
+}
+
+// Bins whose |nu| reaches 2^19 cycles (f_k within ~0.3 MHz of DC at 100 TECU -- far outside the
+// model's validity, but accepted by the ABI) take the exact binary64 path below: there the
+// FP32-pair product (~2^-46 relative) would leave > 1e-8 cycles of phase error.
+constexpr float kPhaseExactCycles = 524288.0f;
+
+// Eq. 15 phase cycles of signed bin kk reduced mod 1, in binary64 with the oracle's operations term
+// for term (f_k = fc + (fs/n) kk, nu = 2 K2 / (c f_k), r = nu - rint(nu); R2-R4), so the result
+// equals the oracle's to the FP32 rounding of r even where |nu| ~ 1e10.  Out of line: rare path.
+static __device__ __noinline__ float phase_frac_exact(double k2, double fc, double fs_over_n, long long kk) {
+  const double f = __dadd_rn(fc, __dmul_rn(fs_over_n, (double)kk));
+  if (!(f > 0.0)) return 0.f;
+  const double nu = __ddiv_rn(__dmul_rn(2.0, k2), __dmul_rn(kC, f));
+  return __double2float_rn(nu - rint(nu));
+}
+
+// phase cycles of bin k of an n-point pulse with table entry g = 1/f_k (FP32 pair): the FP32-pair
+// product, or the exact binary64 path for huge |nu| (signed bin index: the Nyquist bin is negative, R2)
+__device__ __forceinline__ float phase_cycles(const PulseParams &pr, float2 g, long long k, long long n, double fc,
+                                              double fs_over_n) {
+  float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
+  if (fabsf(pr.nu_hi * g.x) >= kPhaseExactCycles) rf = phase_frac_exact(pr.k2, fc, fs_over_n, k >= n / 2 ? k - n : k);
+  return rf;
 }
 
 // ----------------------------------------------------------------------------- complex float

@@ -97,23 +97,4 @@ struct DopplerArgs {
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
 int doppler_path(double max_abs_beta_m1, bool taper = false);
 
-// one persistent kernel for dc_correct of 2^20-sample pulses (fused_correct.cu)
-struct FusedLaunch {
-  const float2 *x;
-  float2 *y;
-  float2 *ring;  // depth * Pg pulses
-  int64_t pulses;
-  int Pg, depth;
-  int lag;    // wavefront steps between dependent stages (depth > 3 lag)
-  int hints;  // L2 policy bits: 1 x loads evict_first, 2 ring stores evict_last, 4 last ring read evict_first
-  const PulseParams *pp;
-  const float2 *tw1024, *gtab;
-  int taps;
-  double carrier;               // fc / fs
-  unsigned long long *sync;     // 8 + 16 * ngroups bytes of scheduler state (zeroed per launch)
-  unsigned long long *stats;    // optional per-CTA cycle counters (tuning only), or null
-  cudaStream_t stream;
-};
-cudaError_t launch_fused_correct(const FusedLaunch &f, double max_abs_beta_m1);
-
 }  // namespace dc

@@ -22,20 +22,20 @@ namespace dc {
 // per-pulse parameters from the raw host arrays (large batches): the host path's binary64
 // arithmetic, term for term (nu_coef = k2c tec, its FP32 hi/lo split, beta = 1 / alpha)
 __global__ void expand_params_kernel(const double *__restrict__ tec, const double *__restrict__ alpha,
-                                     PulseParams *__restrict__ out, int64_t batch, double k2c) {
+                                     PulseParams *__restrict__ out, int64_t batch, double k2c, double k2pt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= batch) return;
   PulseParams q;
   q.nu_coef = tec ? __dmul_rn(k2c, tec[i]) : 0.0;
+  q.k2 = tec ? __dmul_rn(k2pt, tec[i]) : 0.0;
   q.nu_hi = __double2float_rn(q.nu_coef);
   q.nu_lo = __double2float_rn(__dsub_rn(q.nu_coef, (double)q.nu_hi));
-  q.pad0 = q.pad1 = 0.f;
   q.beta = alpha ? __ddiv_rn(1.0, alpha[i]) : 1.0;
   out[i] = q;
 }
 cudaError_t launch_expand_params(const double *tec, const double *alpha, PulseParams *out, int64_t batch, double k2c,
-                                 cudaStream_t st) {
-  expand_params_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(tec, alpha, out, batch, k2c);
+                                 double k2pt, cudaStream_t st) {
+  expand_params_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(tec, alpha, out, batch, k2c, k2pt);
   return cudaGetLastError();
 }
 }  // namespace dc
@@ -105,22 +105,9 @@ struct dc_plan_s {
   dc::TaperCoef tc{};
   int taper_terms = dc::kTaperTerms;
   bool ref_set = false;
-  float2 *scratch = nullptr;  // chunk * n samples
-  float2 *scratch2 = nullptr;  // second chunk buffer (two chunks in flight on the internal streams)
+  float2 *scratch = nullptr;  // launch-group buffer of dc_correct: chunk * n samples
   int64_t scratch_bytes = 0;
-  // chunk pipelining: consecutive chunks alternate between two internal streams, each kernel
-  // capped at half the SMs, so memory-bound and compute-bound passes of different chunks co-run
-  cudaStream_t ws[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
-  bool pipeline = false;  // DISPCORR_PIPE=1 enables (measured slower with large chunks; kept for tuning)
-  // fused persistent dc_correct (n = 2^20): L2-sized groups through a ring of `fdepth` groups
-  // opt-in (DISPCORR_FUSED=1): measured 44.7 GS/s vs 55.6 for the multi-kernel path -- the stages
-  // are compute-bound, so saving the intermediate HBM round trips does not pay yet
-  bool fused = false;
-  int fpg = 1, fdepth = 8, flag = 2, fhints = 7;  // ring of fdepth groups; wavefront lag; L2 policy bits
-  float2 *fring = nullptr;
-  unsigned long long *fsync = nullptr;
-  int64_t fsync_groups = 0;
+  cudaEvent_t ev_stream = nullptr;  // dc_set_stream: orders the new stream after the old one
   // host-path buffers (lazily allocated)
   float2 *hin[2] = {nullptr, nullptr}, *hout[2] = {nullptr, nullptr};
   int64_t host_chunk = 0;
@@ -269,7 +256,7 @@ dc_status stage_params(dc_plan_s *p, int64_t batch, const double *tec, const dou
       DC_CUDA(cudaMemcpyAsync(s.dev_raw + batch, raw + batch, sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream),
               "cudaMemcpyAsync(params)");
     DC_CUDA(dc::launch_expand_params(tec ? s.dev_raw : nullptr, alpha ? s.dev_raw + batch : nullptr, s.dev, batch, k2c,
-                                     p->stream),
+                                     dc::k2_per_tec(), p->stream),
             "expand_params_kernel launch");
     *dev = s.dev;
     *slot_out = &s;
@@ -278,9 +265,9 @@ dc_status stage_params(dc_plan_s *p, int64_t batch, const double *tec, const dou
   }
   for (int64_t i = 0; i < batch; ++i) {
     s.host[i].nu_coef = tec ? k2c * tec[i] : 0.0;
+    s.host[i].k2 = tec ? dc::k2_per_tec() * tec[i] : 0.0;  // the oracle's K2 (orc_iono_phase_cycles)
     s.host[i].nu_hi = (float)s.host[i].nu_coef;
     s.host[i].nu_lo = (float)(s.host[i].nu_coef - (double)s.host[i].nu_hi);
-    s.host[i].pad0 = s.host[i].pad1 = 0.f;
     s.host[i].beta = alpha ? 1.0 / alpha[i] : 1.0;
     mb = std::max(mb, std::fabs(s.host[i].beta - 1.0));
   }
@@ -296,6 +283,17 @@ dc_status release_slot(dc_plan_s *p, ParamSlot *s) {
   DC_CUDA(cudaEventRecord(s->done, p->stream), "cudaEventRecord(param slot)");
   s->used = true;
   return DC_OK;
+}
+
+// release a staged slot on every exit path after stage_params (also when a launch failed: the
+// slot's event then marks whatever was enqueued); returns the first error
+dc_status release_after(dc_plan_s *p, ParamSlot *slot, dc_status s) {
+  if (s != DC_OK) {
+    cudaEventRecord(slot->done, p->stream);
+    slot->used = true;
+    return s;
+  }
+  return release_slot(p, slot);
 }
 
 // ---- profiling brackets ----------------------------------------------------------------------------
@@ -330,11 +328,29 @@ struct ProfScope {
   }
 };
 
-// where a chunk's kernels go: stream + persistent-grid cap
+// where a launch group's kernels go: stream + persistent-grid cap (0 = one wave of the whole GPU)
 struct Lane {
   cudaStream_t st;
   int cap;
 };
+
+// Every entry point that touches the device makes the plan's device current and restores the
+// caller's device on return (a multi-GPU process keeps its own current device).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+#define DC_DEVICE_GUARD(p)                                              \
+  DeviceGuard dev_guard_(p->device);                                    \
+  if (dev_guard_.err != cudaSuccess) return cuda_fail(dev_guard_.err, "cudaSetDevice")
 
 // ---- stage launchers (no validation) -----------------------------------------------------------
 // var: 0 Eq. 15, 1 Eq. 14, 2 Eq. 15 + matched filter, 3 conj reference spectrum into p->ref
@@ -385,50 +401,21 @@ bool compress_supported(const dc_plan_s *p) {
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                       int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
-  int cap = ln.cap;
-  if (const char *env = getenv("DISPCORR_DOP_CAP")) cap = atoi(env);  // tuning experiments only
-  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, cap, p->taper, p->tc, p->taper_terms};
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, ln.cap, p->taper, p->tc, p->taper_terms};
   ProfScope ps(p, DC_K_DOPPLER, pulses * p->n, ln.st);
   DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
   return DC_OK;
 }
 
-// internal streams wait for everything enqueued so far on the plan stream; afterwards the plan
-// stream waits for both internal streams (so callers see ordinary stream semantics)
-dc_status fork(dc_plan_s *p) {
-  if (!p->ws[0]) {
-    for (int i = 0; i < 2; ++i) {
-      DC_CUDA(cudaStreamCreateWithFlags(&p->ws[i], cudaStreamNonBlocking), "cudaStreamCreate");
-      DC_CUDA(cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming), "cudaEventCreate");
-    }
-    DC_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
-  }
-  DC_CUDA(cudaEventRecord(p->ev_fork, p->stream), "cudaEventRecord(fork)");
-  for (int i = 0; i < 2; ++i) DC_CUDA(cudaStreamWaitEvent(p->ws[i], p->ev_fork, 0), "cudaStreamWaitEvent(fork)");
-  return DC_OK;
-}
-dc_status join(dc_plan_s *p) {
-  for (int i = 0; i < 2; ++i) {
-    DC_CUDA(cudaEventRecord(p->ev_join[i], p->ws[i]), "cudaEventRecord(join)");
-    DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join[i], 0), "cudaStreamWaitEvent(join)");
-  }
-  return DC_OK;
-}
-
-// launch-group buffer(s) for dc_correct: one, or two for the two-stream schedule; min(chunk, batch) pulses each
+// launch-group buffer for dc_correct: min(chunk, batch) pulses
 dc_status ensure_scratch(dc_plan_s *p, int64_t batch) {
   const int64_t need = std::min(p->chunk, batch) * p->n * (int64_t)sizeof(float2);
   if (p->scratch_bytes >= need) return DC_OK;
   DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize(scratch)");
-  for (int i = 0; i < 2; ++i)
-    if (p->ws[i]) DC_CUDA(cudaStreamSynchronize(p->ws[i]), "cudaStreamSynchronize(scratch)");
   if (p->scratch) cudaFree(p->scratch);
-  if (p->scratch2) cudaFree(p->scratch2);
-  p->scratch = p->scratch2 = nullptr;
+  p->scratch = nullptr;
   p->scratch_bytes = 0;
-  // the second group buffer is only used by the two-stream schedule (DISPCORR_PIPE=1)
-  if (cudaMalloc(&p->scratch, (size_t)need) != cudaSuccess ||
-      (p->pipeline && cudaMalloc(&p->scratch2, (size_t)need) != cudaSuccess)) {
+  if (cudaMalloc(&p->scratch, (size_t)need) != cudaSuccess) {
     cudaGetLastError();
     return fail(DC_ERR_OUT_OF_MEMORY, "launch-group buffer(s) of %lld bytes", (long long)need);
   }
@@ -452,23 +439,18 @@ dc_status iono_common(dc_plan_t p, const void *x, void *z, int64_t batch, const 
       return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^14 .. 2^21 (plan n = %lld)", (long long)p->n);
     if (!p->ref_set) return fail(DC_ERR_INVALID_VALUE, "no matched-filter reference: call dc_set_reference first");
   }
-  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_DEVICE_GUARD(p);
   PulseParams *pp;
   ParamSlot *slot;
   if ((s = stage_params(p, batch, tec, nullptr, &pp, &slot, nullptr)) != DC_OK) return s;
   const float2 *xp = (const float2 *)x;
   float2 *zp = (float2 *)z;
   const int64_t step = (p->regime == 0) ? std::min<int64_t>(batch, 1ll << 30) : p->chunk;
-  const int64_t nchunks = (batch + step - 1) / step;
-  const bool pipe = nchunks > 1 && !p->prof && p->pipeline;
-  if (pipe && (s = fork(p)) != DC_OK) return s;
-  for (int64_t b0 = 0, i = 0; b0 < batch; b0 += step, ++i) {
+  for (int64_t b0 = 0; b0 < batch && s == DC_OK; b0 += step) {
     const int64_t nb = std::min(step, batch - b0);
-    const Lane ln = pipe ? Lane{p->ws[i & 1], (p->sm_count + 1) / 2} : Lane{p->stream, 0};
-    if ((s = run_iono(p, xp + b0 * p->n, zp + b0 * p->n, nb, pp, b0, var, ln)) != DC_OK) return s;
+    s = run_iono(p, xp + b0 * p->n, zp + b0 * p->n, nb, pp, b0, var, Lane{p->stream, 0});
   }
-  if (pipe && (s = join(p)) != DC_OK) return s;
-  return release_slot(p, slot);
+  return release_after(p, slot, s);
 }
 
 }  // namespace
@@ -520,7 +502,8 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
   if (prop.major != 10 || prop.minor != 0)
     return fail(DC_ERR_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; libdispcorr is built for sm_100a (B200)", device,
                 prop.major, prop.minor);
-  DC_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  DeviceGuard dg(device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
 
   dc_plan_s *p = new (std::nothrow) dc_plan_s();
   if (!p) return fail(DC_ERR_OUT_OF_MEMORY, "plan allocation");
@@ -581,12 +564,7 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     if ((s = upload(&p->twl, lo)) != DC_OK) return cleanup(s);
     if ((s = upload(&p->twh, hi)) != DC_OK) return cleanup(s);
   }
-  int64_t target = kChunkTargetBytes;
-  if (const char *env = getenv("DISPCORR_CHUNK_MB")) {  // tuning override (benchmarks only)
-    const long v = atol(env);
-    if (v > 0) target = (int64_t)v << 20;
-  }
-  p->chunk = std::max<int64_t>(1, target / (n * (int64_t)sizeof(float2)));
+  p->chunk = std::max<int64_t>(1, kChunkTargetBytes / (n * (int64_t)sizeof(float2)));
   // per-bin g_k = 1/f_k (0 where f_k <= 0, reading R3) for the warp-level row kernel, FP32 pairs:
   // regime 0 (n = 1024): natural bin order; four-step with N2 = 1024: row layout [k1][k2] of k = k1 + N1 k2
   if (p->tw1024) {
@@ -603,50 +581,40 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
       }
     if ((s = upload(&p->gtab, g)) != DC_OK) return cleanup(s);
   }
-  if (const char *env = getenv("DISPCORR_PIPE")) p->pipeline = atoi(env) != 0;
-  if (const char *env = getenv("DISPCORR_FUSED")) p->fused = atoi(env) != 0;
-  if (const char *env = getenv("DISPCORR_FUSED_PG")) p->fpg = std::max(1, atoi(env));
-  if (const char *env = getenv("DISPCORR_FUSED_LAG")) p->flag = std::max(1, atoi(env));
-  p->fdepth = 3 * p->flag + 2;
-  if (const char *env = getenv("DISPCORR_FUSED_DEPTH")) p->fdepth = std::max(3 * p->flag + 1, atoi(env));
-  if (const char *env = getenv("DISPCORR_FUSED_HINTS")) p->fhints = atoi(env);
   p->chunk = std::min<int64_t>(p->chunk, 65535);
   p->scratch_bytes = 0;  // chunk buffers are allocated on first use, sized to the batch (ensure_scratch)
   for (auto &slot : p->ring)
     if (cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
+  if (cudaEventCreateWithFlags(&p->ev_stream, cudaEventDisableTiming) != cudaSuccess)
+    return cleanup(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
   *out = p;
   return DC_OK;
 }
 
 dc_status dc_plan_destroy(dc_plan_t p) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
-  cudaSetDevice(p->device);
+  DeviceGuard dg(p->device);
   cudaStreamSynchronize(p->stream);
-  for (int i = 0; i < 2; ++i) {
-    if (p->ws[i]) cudaStreamSynchronize(p->ws[i]);
-  }
-  if (p->fsync) cudaFree(p->fsync);
-  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw_w1024, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl, p->scratch, p->scratch2, p->gtab, p->fring, p->ref,
-                    p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
+  if (p->s_h2d) cudaStreamSynchronize(p->s_h2d);
+  if (p->s_d2h) cudaStreamSynchronize(p->s_d2h);
+  float2 *bufs[] = {p->tw_small_f, p->tw_small_i, p->tw_w1024, p->tw1f, p->tw1i, p->tw2f, p->tw2i, p->twh, p->twl,
+                    p->scratch, p->gtab, p->ref, p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
   for (float2 *b : bufs)
     if (b) cudaFree(b);
   for (auto &s : p->ring) {
     if (s.done) cudaEventDestroy(s.done);
     if (s.host) cudaFreeHost(s.host);
     if (s.dev) cudaFree(s.dev);
+    if (s.dev_raw) cudaFree(s.dev_raw);
   }
+  if (p->ev_stream) cudaEventDestroy(p->ev_stream);
   for (int i = 0; i < 2; ++i) {
     if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
     if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
     if (p->ev_out[i]) cudaEventDestroy(p->ev_out[i]);
   }
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i) {
-    if (p->ws[i]) cudaStreamDestroy(p->ws[i]);
-    if (p->ev_join[i]) cudaEventDestroy(p->ev_join[i]);
-  }
-  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
   if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
   delete p;
@@ -655,13 +623,19 @@ dc_status dc_plan_destroy(dc_plan_t p) {
 
 dc_status dc_set_stream(dc_plan_t p, void *stream) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  if ((cudaStream_t)stream == p->stream) return DC_OK;
+  DC_DEVICE_GUARD(p);
+  // work already enqueued on the old stream still reads / writes plan-owned buffers (scratch,
+  // reference table, parameter ring): the new stream waits for it before any later call runs
+  DC_CUDA(cudaEventRecord(p->ev_stream, p->stream), "cudaEventRecord(set_stream)");
+  DC_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, p->ev_stream, 0), "cudaStreamWaitEvent(set_stream)");
   p->stream = (cudaStream_t)stream;
   return DC_OK;
 }
 
 dc_status dc_sync(dc_plan_t p) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
-  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_DEVICE_GUARD(p);
   DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
   return DC_OK;
 }
@@ -681,7 +655,7 @@ dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
     return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^14 .. 2^21 (plan n = %lld)", (long long)p->n);
   if (L < 1 || L > p->n) return fail(DC_ERR_INVALID_VALUE, "reference length L = %lld must be in [1, n = %lld]", (long long)L, (long long)p->n);
   if ((s = check_device_ptr(p, r, "r")) != DC_OK) return s;
-  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_DEVICE_GUARD(p);
   if (!p->ref && cudaMalloc(&p->ref, (size_t)p->n * sizeof(float2)) != cudaSuccess) {
     cudaGetLastError();
     p->ref = nullptr;
@@ -736,18 +710,18 @@ dc_status dc_doppler(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   if ((s = check_device_ptr(p, y, "y")) != DC_OK) return s;
   if ((s = check_overlap(x, y, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
   if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
-  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_DEVICE_GUARD(p);
   PulseParams *pp;
   ParamSlot *slot;
   double mb = 0;
   if ((s = stage_params(p, batch, nullptr, alpha, &pp, &slot, &mb)) != DC_OK) return s;
   const float2 *xp = (const float2 *)x;
   float2 *yp = (float2 *)y;
-  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+  for (int64_t b0 = 0; b0 < batch && s == DC_OK; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, batch - b0);
-    if ((s = run_doppler(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
+    s = run_doppler(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb, Lane{p->stream, 0});
   }
-  return release_slot(p, slot);
+  return release_after(p, slot, s);
 }
 
 dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const double *tec, const double *alpha) {
@@ -759,7 +733,7 @@ dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   if ((s = check_overlap(x, y, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
   if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
-  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_DEVICE_GUARD(p);
   if ((s = ensure_scratch(p, batch)) != DC_OK) return s;
   PulseParams *pp;
   ParamSlot *slot;
@@ -767,63 +741,13 @@ dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   if ((s = stage_params(p, batch, tec, alpha, &pp, &slot, &mb)) != DC_OK) return s;
   const float2 *xp = (const float2 *)x;
   float2 *yp = (float2 *)y;
-  if (p->fused && !p->taper && p->log2n == 20 && p->regime == 1 && p->tw1024 && p->gtab && dc::doppler_path(mb) != 0) {
-    // one persistent kernel: groups of fpg pulses through an L2-sized ring (fused_correct.cu)
-    const int64_t ngroups = (batch + p->fpg - 1) / p->fpg;
-    if (!p->fring) {
-      if (cudaMalloc(&p->fring, (size_t)p->fpg * p->fdepth * p->n * sizeof(float2)) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DC_ERR_OUT_OF_MEMORY, "fused ring buffer");
-      }
-    }
-    if (p->fsync_groups < ngroups) {
-      if (p->fsync) cudaFree(p->fsync);
-      p->fsync = nullptr;
-      if (cudaMalloc(&p->fsync, sizeof(unsigned long long) + 16 * (size_t)ngroups) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DC_ERR_OUT_OF_MEMORY, "fused scheduler state");
-      }
-      p->fsync_groups = ngroups;
-    }
-    unsigned long long *stats = nullptr;
-    const bool want_stats = getenv("DISPCORR_FUSED_STATS") != nullptr;  // tuning only: per-CTA cycle split
-    if (want_stats) {
-      if (cudaMalloc(&stats, 148 * 16 * 8) != cudaSuccess) return fail(DC_ERR_OUT_OF_MEMORY, "stats");
-      cudaMemsetAsync(stats, 0, 148 * 16 * 8, p->stream);
-    }
-    dc::FusedLaunch f{xp, yp, p->fring, batch, p->fpg, p->fdepth, p->flag, p->fhints, pp, p->tw1024, p->gtab, p->taps, p->fc / p->fs,
-                      p->fsync, stats, p->stream};
-    {
-      ProfScope ps(p, DC_K_FUSED, batch * p->n, p->stream);
-      DC_CUDA(dc::launch_fused_correct(f, mb), "fused_correct_kernel launch");
-    }
-    if (want_stats) {
-      unsigned long long h[148 * 16];
-      cudaMemcpyAsync(h, stats, sizeof h, cudaMemcpyDeviceToHost, p->stream);
-      cudaStreamSynchronize(p->stream);
-      cudaFree(stats);
-      double t[16] = {0};
-      for (int b = 0; b < 148; ++b)
-        for (int k = 0; k < 16; ++k) t[k] += (double)h[b * 16 + k] / 148.0;
-      fprintf(stderr,
-              "fused stats (mean cycles per CTA): wait_full %.0f  A %.0f  B %.0f  C %.0f  D %.0f  items %.0f+%.0f  "
-              "producer dep %.0f free %.0f\n",
-              t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[8], t[9]);
-    }
-    return release_slot(p, slot);
-  }
-  const int64_t nchunks = (batch + p->chunk - 1) / p->chunk;
-  const bool pipe = nchunks > 1 && !p->prof && p->pipeline;
-  if (pipe && (s = fork(p)) != DC_OK) return s;
-  for (int64_t b0 = 0, i = 0; b0 < batch; b0 += p->chunk, ++i) {
+  const Lane ln{p->stream, 0};
+  for (int64_t b0 = 0; b0 < batch && s == DC_OK; b0 += p->chunk) {
     const int64_t nb = std::min(p->chunk, batch - b0);
-    const Lane ln = pipe ? Lane{p->ws[i & 1], (p->sm_count + 1) / 2} : Lane{p->stream, 0};
-    float2 *scr = (pipe && (i & 1)) ? p->scratch2 : p->scratch;
-    if ((s = run_iono(p, xp + b0 * p->n, scr, nb, pp, b0, false, ln)) != DC_OK) return s;
-    if ((s = run_doppler(p, scr, yp + b0 * p->n, nb, pp, b0, mb, ln)) != DC_OK) return s;
+    s = run_iono(p, xp + b0 * p->n, p->scratch, nb, pp, b0, 0, ln);
+    if (s == DC_OK) s = run_doppler(p, p->scratch, yp + b0 * p->n, nb, pp, b0, mb, ln);
   }
-  if (pipe && (s = join(p)) != DC_OK) return s;
-  return release_slot(p, slot);
+  return release_after(p, slot, s);
 }
 
 dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t batch, const double *tec,
@@ -836,7 +760,7 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
   if ((s = check_overlap(x_host, y_host, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
   if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
-  DC_CUDA(cudaSetDevice(p->device), "cudaSetDevice");
+  DC_DEVICE_GUARD(p);
   // pulses per transfer chunk: bounded so the pinned-host pipeline overlaps (~64 MiB per copy)
   const int64_t hc = std::max<int64_t>(1, std::min(p->chunk, (int64_t)(64ll << 20) / (p->n * (int64_t)sizeof(float2))));
   {
@@ -875,25 +799,29 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
   char *yh = (char *)y_host;
   const size_t pulse_bytes = (size_t)p->n * sizeof(float2);
   // 3-stage pipeline: H2D (s_h2d) -> correct (plan stream) -> D2H (s_d2h), double-buffered
-  int64_t it = 0;
-  for (int64_t b0 = 0; b0 < batch; b0 += hc, ++it) {
-    const int i = (int)(it & 1);
-    const int64_t nb = std::min(hc, batch - b0);
-    if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_comp[i], 0), "wait");  // hin[i] free
-    DC_CUDA(cudaMemcpyAsync(p->hin[i], xh + b0 * pulse_bytes, nb * pulse_bytes, cudaMemcpyHostToDevice, p->s_h2d),
-            "cudaMemcpyAsync(H2D)");
-    DC_CUDA(cudaEventRecord(p->ev_in[i], p->s_h2d), "record");
-    DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[i], 0), "wait");
-    if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[i], 0), "wait");  // hout[i] drained
-    if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, false, Lane{p->stream, 0})) != DC_OK) return s;
-    if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
-    DC_CUDA(cudaEventRecord(p->ev_comp[i], p->stream), "record");
-    DC_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[i], 0), "wait");
-    DC_CUDA(cudaMemcpyAsync(yh + b0 * pulse_bytes, p->hout[i], nb * pulse_bytes, cudaMemcpyDeviceToHost, p->s_d2h),
-            "cudaMemcpyAsync(D2H)");
-    DC_CUDA(cudaEventRecord(p->ev_out[i], p->s_d2h), "record");
-  }
-  if ((s = release_slot(p, slot)) != DC_OK) return s;
+  auto pipeline = [&]() -> dc_status {
+    int64_t it = 0;
+    for (int64_t b0 = 0; b0 < batch; b0 += hc, ++it) {
+      const int i = (int)(it & 1);
+      const int64_t nb = std::min(hc, batch - b0);
+      if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_comp[i], 0), "wait");  // hin[i] free
+      DC_CUDA(cudaMemcpyAsync(p->hin[i], xh + b0 * pulse_bytes, nb * pulse_bytes, cudaMemcpyHostToDevice, p->s_h2d),
+              "cudaMemcpyAsync(H2D)");
+      DC_CUDA(cudaEventRecord(p->ev_in[i], p->s_h2d), "record");
+      DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[i], 0), "wait");
+      if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[i], 0), "wait");  // hout[i] drained
+      if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, false, Lane{p->stream, 0})) != DC_OK) return s;
+      if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
+      DC_CUDA(cudaEventRecord(p->ev_comp[i], p->stream), "record");
+      DC_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[i], 0), "wait");
+      DC_CUDA(cudaMemcpyAsync(yh + b0 * pulse_bytes, p->hout[i], nb * pulse_bytes, cudaMemcpyDeviceToHost, p->s_d2h),
+              "cudaMemcpyAsync(D2H)");
+      DC_CUDA(cudaEventRecord(p->ev_out[i], p->s_d2h), "record");
+    }
+    return DC_OK;
+  };
+  s = release_after(p, slot, pipeline());
+  if (s != DC_OK) return s;
   DC_CUDA(cudaStreamSynchronize(p->s_d2h), "cudaStreamSynchronize(D2H)");
   DC_CUDA(cudaStreamSynchronize(p->stream), "cudaStreamSynchronize");
   return DC_OK;
@@ -943,7 +871,7 @@ dc_status dc_plan_info(dc_plan_t p, dc_plan_info_t *info) {
   info->n1 = p->regime ? (1ll << p->P1) : 0;
   info->n2 = p->regime ? (1ll << p->P2) : 0;
   info->chunk_pulses = p->chunk;
-  info->scratch_bytes = (p->pipeline ? 2 : 1) * p->scratch_bytes;
+  info->scratch_bytes = p->scratch_bytes;
   info->sm_count = p->sm_count;
   info->kernel_launches = p->launches;
   return DC_OK;

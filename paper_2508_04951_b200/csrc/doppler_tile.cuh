@@ -205,6 +205,8 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
     if constexpr (TAPER > 0) {
       float K, dK;
       kaiser_taper<TAPER>(*tcp, d, K, dK);
+      // the taper's centre weight is 1 exactly (R17): the FP32 Horner sum need not round to 1
+      if (TINY && d == 0.f) K = 1.f;
       w1 = fmaf(w1, K, w * dK);
       w *= K;
     }

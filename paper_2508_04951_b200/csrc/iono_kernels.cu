@@ -56,11 +56,6 @@ constexpr bool kRowStage = (DC_ROW_NW <= 12);
 static size_t warp_row_smem(int log2n, int H, bool outer) {
   return RowCfg<DC_ROW_NW, kRowStage>::elems(outer, log2n, H) * sizeof(float2);
 }
-static size_t warp_col_smem(int log2n, int H, bool outer) {
-  (void)outer, (void)log2n, (void)H;  // outer twiddles come from twn(): no table staged
-  const size_t e = (size_t)2 * 1024 * 8 + (size_t)kWW * (kWPad + 32) + 1024;
-  return e * sizeof(float2) + 2 * sizeof(uint64_t) + 1024;  // + mbarriers, alignment slack
-}
 template <class K>
 static cudaError_t launch_persistent(K kern, size_t smem, int64_t total, const WarpArgs &a, cudaStream_t st, int cap,
                                      int nw = kWW) {
@@ -93,7 +88,6 @@ static cudaError_t launch_warp_row(const WarpArgs &a, bool small, int var, cudaS
 }
 static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st, int cap) {
   const int64_t total = a.pulses * ((1ll << (a.log2n - 10)) / kWW);
-  const size_t smem = warp_col_smem(a.log2n, a.H, !inv);
   // source tensor {t2, t1, pulse} of 8-byte samples, box {8 columns, 256 rows, 1}, 64-byte swizzle
   CUtensorMap smap;
   const int n2 = 1 << (a.log2n - 10);
@@ -101,26 +95,14 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
   const uint64_t strides[2] = {(uint64_t)n2 * sizeof(float2), (uint64_t)a.pulse_stride * sizeof(float2)};
   const uint32_t box[3] = {(uint32_t)kWW, 256, 1};
   if (!encode_tile_map(&smap, a.src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
-#ifndef DC_COL_V1
-  const size_t smem2 = warp_col3_smem_bytes();
-  (void)smem;
+  const size_t launch_smem = warp_col3_smem_bytes();
   auto kern = inv ? warp_col3_kernel<true> : warp_col3_kernel<false>;
   constexpr int threads = 2 * kWW * 32;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-#else
-  auto kern = inv ? warp_col_kernel<true> : warp_col_kernel<false>;
-  constexpr int threads = kWW * 32;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-#endif
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)launch_smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#ifndef DC_COL_V1
-  const size_t launch_smem = smem2;
-#else
-  const size_t launch_smem = smem;
-#endif
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, launch_smem);
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);

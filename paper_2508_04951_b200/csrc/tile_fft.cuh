@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
           float2 m = make_float2(inv_n, 0.f);
           if (f > 0.0 && nu_coef != 0.0) {
             const double nu = nu_coef * drcp(f);
-            const float rf = __double2float_rn(nu - rint(nu));
+            float rf = __double2float_rn(nu - rint(nu));
+            if (fabs(nu) >= (double)kPhaseExactCycles)  // huge |nu|: the oracle's binary64 operations
+              rf = phase_frac_exact(a.pp[a.pulse_base + p].k2, a.fc, a.fs_over_n, kk);
             const float2 w = expm2pi(DISTORT ? -rf : rf);
             m = make_float2(w.x * inv_n, w.y * inv_n);
           }

@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
         for (int s = 0; s < 32; ++s) {
           if (!SG && s % 8 == 0) asm volatile("" ::: "memory");  // table loads in chunks of 8 (registers)
           const float2 g = SG ? grow[lane + 32 * s] : __ldg(grow + lane + 32 * s);
-          const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
+          const uint32_t kb = (MODE == MODE_ROWB) ? k1 + ((uint32_t)(lane + 32 * s) << P1) : (uint32_t)(lane + 32 * s);
+          const float rf = phase_cycles(pr, g, kb, n, a.fc, a.fs_over_n);
           const float2 w = expm2pi((VAR == VAR_DISTORT) ? -rf : rf);
           v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
           if constexpr (VAR == VAR_COMPRESS) v[s] = cmul(v[s], rc[s]);
@@ -240,97 +241,14 @@ __device__ __forceinline__ int col_sw(int row, int col) {
 // Staging: the TMA engine loads the [1024][8] tile as four 256-row boxes of a 3-D tensor map
 // {t2 (n2), t1 (1024), pulse} with SWIZZLE_64B, which is exactly the col_sw() layout (16-byte
 // chunk index XOR address bits 7-8), so column reads are 2-way and no LSU instructions are spent
-// on staging.  Two staging buffers (2 tiles in flight), one transaction mbarrier each.
-template <bool INV>
-__global__ void __launch_bounds__(kWW * 32, 1) warp_col_kernel(const WarpArgs a, const __grid_constant__ CUtensorMap smap) {
-  pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
-  extern __shared__ __align__(1024) float4 smem4[];
-  float2 *sm = reinterpret_cast<float2 *>(smem4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  float2 *stg0 = sm;                                   // 2 x [1024][8] swizzled staging tiles
-  float2 *wkall = sm + 2 * 1024 * 8;                   // per-warp exchange buffers
-  float2 *wk = wkall + warp * kWPad;
-  float2 *Pw = wkall + kWW * kWPad + warp * 32;
-  float4 *Tw = reinterpret_cast<float4 *>(wkall + kWW * (kWPad + 32));
-  const int log2n = a.log2n;
-  const int n = 1 << log2n;
-  const uint32_t nmask = (uint32_t)n - 1u;
-  const int n2 = n >> 10;
-  const int64_t tiles_per_pulse = n2 / kWW;
-  const int64_t total = a.pulses * tiles_per_pulse;
-
-  for (int i = tid; i < 512; i += kWW * 32) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(Tw + 512);  // outer twiddles come from twn(): no table
-  auto stage = [&](int64_t it, float2 *stg, uint64_t *bar) {  // thread 0 only
-    const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
-    fence_proxy_async();
-    mbar_arrive_expect_tx(bar, 1024 * 8 * sizeof(float2));
-#pragma unroll
-    for (int b = 0; b < 4; ++b) tma_load_3d(stg + b * 256 * 8, &smap, (int)c0, b * 256, (int)p, bar);
-  };
-  // two tiles in flight: tile i computes while tiles i+1 and i+2 stream in
-  int64_t it = blockIdx.x;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_fence_init();
-    if (it < total) stage(it, stg0, &bars[0]);
-    if (it + gridDim.x < total) stage(it + gridDim.x, stg0 + 8192, &bars[1]);
-  }
-  __syncthreads();  // tables and barrier initialisation visible
-  int bsel = 0;
-  unsigned phase[2] = {0u, 0u};
-
-  for (; it < total; it += gridDim.x, bsel ^= 1) {
-    float2 *stg = stg0 + bsel * 8192;
-    mbar_wait(&bars[bsel], phase[bsel]);
-    phase[bsel] ^= 1u;
-    float2 v[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) v[r] = stg[col_sw(lane + 32 * r, warp)];
-    __syncthreads();  // staging tile free
-    const int64_t nit = it + 2 * (int64_t)gridDim.x;
-    if (tid == 0 && nit < total) stage(nit, stg, &bars[bsel]);
-    const int64_t p = it / tiles_per_pulse, c0 = (it - p * tiles_per_pulse) * kWW;
-
-    if constexpr (!INV) {
-      wfft1024<false>(v, wk, Tw, lane);
-      // outputs k1 = lane + 32 s of column t2: times w_n^(k1 t2)
-      const uint32_t t2 = (uint32_t)(c0 + warp);
-      __syncwarp();
-      Pw[lane] = twn((32u * t2 * (uint32_t)lane) & nmask, log2n);
-      // the 1/n of the inverse transform (R6) is folded into pass A's twiddle
-      const float2 base = cscale(twn((t2 * (uint32_t)lane) & nmask, log2n), a.scale);
-      __syncwarp();
-#pragma unroll
-      for (int s = 0; s < 32; ++s) v[s] = cmul(v[s], cmul(base, Pw[s]));
-    } else {
-      wfft1024<true>(v, wk, Tw, lane);
-    }
-    // column (in natural row order lane + 32 s) -> own exchange buffer, then cooperative store
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < 32; ++s) wk[wpad(lane + 32 * s)] = v[s];
-    __syncthreads();
-    float2 *g = a.dst + p * a.pulse_stride + c0;
-#pragma unroll 4
-    for (int i = tid; i < 1024 * 4; i += kWW * 32) {
-      const int row = i >> 2, v4 = i & 3;
-      const float2 e0 = wkall[(2 * v4) * kWPad + wpad(row)];
-      const float2 e1 = wkall[(2 * v4 + 1) * kWPad + wpad(row)];
-      __stcg(reinterpret_cast<float4 *>(g + (int64_t)row * n2 + 2 * v4), make_float4(e0.x, e0.y, e1.x, e1.y));
-    }
-    __syncthreads();  // exchange buffers free before the next tile's FFT reuses them
-  }
-}
-
+// on staging.
 // Column pass, default variant: one CTA of TWO 8-warp consumer groups per SM and THREE staging
 // slots.  Local tile i of the CTA goes to group i mod 2 and slot i mod 3; a slot holds the 64 KiB
 // [1024][8] tile and is then reused in place as its group's padded exchange space (8 x 1058
 // samples), so the CTA needs 3 x 68 KiB.  When group g finishes tile i (tile stored, group
 // barrier) it issues the TMA load of tile i + 3 into the freed slot, so two tiles are computed
-// while the third streams in.  (warp_col_kernel above: one 8-warp group, two staging tiles plus
-// separate exchange buffers -- 8 warps per SM and the load latency exposed between tiles.)
+// while the third streams in.  (The round-1 single-group variant -- one 8-warp group, two staging
+// tiles plus separate exchange buffers -- left the load latency exposed between tiles: 64 / 71 %.)
 constexpr int kColSlot = ((kWW * kWPad * 8 + 1023) / 1024) * 1024 / 8;  // float2 elements
 constexpr int kColSlots = 3;
 __host__ __device__ constexpr size_t warp_col3_smem_bytes() {

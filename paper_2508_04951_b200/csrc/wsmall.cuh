@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(kWsT, 1) warp_small_kernel(const WarpArgs a) {
 #pragma unroll
       for (int s = 0; s < 32; ++s) {
         if (s % 8 == 0) asm volatile("" ::: "memory");  // table loads in chunks of 8 (registers)
-        const float rf = phase_frac(pr.nu_hi, pr.nu_lo, __ldg(grow + lane + 32 * s));
+        const float rf = phase_cycles(pr, __ldg(grow + lane + 32 * s), k1 + (int64_t)N1 * (lane + 32 * s), n, a.fc,
+                                      a.fs_over_n);
         v[s] = cmul(v[s], expm2pi((VAR == VAR_DISTORT) ? -rf : rf));
       }
       wfft1024<true>(v, wk, Tw, lane);

@@ -17,7 +17,8 @@ TECU = 1e16                 # 1 TEC unit in electrons / m^2
 BANK_SEED = 4951
 PARAM_SEED = 4952
 # alpha range for |v| <= 5 km/s (Eq. 13 with v = +-5000 m/s): 1 +- 3.33569658541e-5
-ALPHA_SPAN_5KMS = 3.33569658541e-5
+ALPHA_SPAN_5KMS = 3.33569658541e-5  # alpha(5 km/s) - 1
+C_LIGHT = 299792458.0
 
 
 def _t(n: int, fs: float) -> np.ndarray:
@@ -203,11 +204,14 @@ def waveform_bank(n: int, fs: float = FS_PAPER, count: int = 16, T: float = 100e
 
 
 def pulse_params(batch: int, seed: int = PARAM_SEED, tec_max_tecu: float = 200.0,
-                 alpha_span: float = ALPHA_SPAN_5KMS) -> tuple[np.ndarray, np.ndarray]:
-    """Per-pulse TEC ~ U[0, tec_max] TECU and alpha ~ U[1 - span, 1 + span] (|v| <= 5 km/s)."""
+                 v_max_mps: float = 5000.0) -> tuple[np.ndarray, np.ndarray]:
+    """SURVEY 8(d) C4 recipe: per-pulse TEC ~ U[0, tec_max] TECU and radial velocity
+    v ~ U[-v_max, +v_max] mapped to alpha = (1 + v/c) / (1 - v/c) (the Doppler model of Eq. 13's
+    context) -- the workload's parameters, not part of the correction."""
     rng = np.random.default_rng(seed)
     tec = rng.uniform(0.0, tec_max_tecu, batch) * TECU
-    alpha = 1.0 + rng.uniform(-alpha_span, alpha_span, batch)
+    v = rng.uniform(-v_max_mps, v_max_mps, batch)
+    alpha = (1.0 + v / C_LIGHT) / (1.0 - v / C_LIGHT)
     return tec, alpha
 
 

@@ -278,32 +278,6 @@ def test_abi_errors_on_gpu(dc):
     assert info["regime"] == 0 and info["n"] == 1024
 
 
-def test_fused_correct_matches_multi_kernel_path(dc, monkeypatch):
-    # n = 2^20 dc_correct runs as one persistent kernel (fused_correct.cu); it must reproduce the
-    # four-kernel path bit for bit (same arithmetic, different schedule), including a partial
-    # last group (batch not a multiple of the group size) and several groups through the ring.
-    import torch
-    n, batch = 1 << 20, 11
-    bank = synth.waveform_bank(n, count=4)
-    tec, alpha = synth.pulse_params(batch)
-    x = torch.from_numpy(bank[np.arange(batch) % 4]).cuda()
-    monkeypatch.setenv("DISPCORR_FUSED", "1")
-    p1 = dc.Plan(n, 2.048e9, 0.0, taps=32)
-    y1 = torch.empty_like(x)
-    p1.correct(x, y1, tec, alpha)
-    p1.sync()
-    assert p1.info()["kernel_launches"] == 1
-    monkeypatch.setenv("DISPCORR_FUSED", "0")
-    p0 = dc.Plan(n, 2.048e9, 0.0, taps=32)
-    y0 = torch.empty_like(x)
-    p0.correct(x, y0, tec, alpha)
-    p0.sync()
-    assert torch.equal(y0, y1)
-    idx = [0, 5, 10]
-    ref = O.run_batch("correct", bank[np.arange(batch) % 4][idx], 2.048e9, 0.0, 32, tec[idx], alpha[idx])
-    assert rel_l2(y1.cpu().numpy()[idx], ref).max() < TOL
-
-
 # ----------------------------------------------------------------------------- pulse compression (NEXT-2)
 def gpu_compress(dc, x, r, fs, fc, tec, inplace=False):
     p = dc.Plan(x.shape[-1], fs, fc, taps=8)

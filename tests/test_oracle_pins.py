@@ -575,3 +575,14 @@ def test_doppler_exact_carrier_term_baseband():
     without = L.matched_filter_loss_db(O.doppler_exact(echo, fs, 0.0, alpha), truth)
     assert with_c < 0.01
     assert without > 0.1
+
+
+def test_doppler_at_equals_whole_pulse_outputs():
+    # the sampled entry point (parity at 2^22..2^24) evaluates exactly the outputs of orc_doppler_win
+    x = synth.complex_gaussian(2048, seed=19)
+    idx = np.array([0, 1, 777, 1024, 2047])
+    for a, kb in ((1 + 3.3e-5, 0.0), (0.93, 0.0), (1.0 - 2e-5, 8.0)):
+        y = O.doppler(x, 32, 51.2e6, 422e6, a, kaiser=kb)
+        assert np.array_equal(O.doppler_at(x, 32, 51.2e6, 422e6, a, idx, kaiser=kb), y[idx])
+    with pytest.raises(RuntimeError):
+        O.doppler_at(x, 32, 51.2e6, 0.0, 1.0, [2048])
