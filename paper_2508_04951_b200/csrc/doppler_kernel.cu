@@ -7,24 +7,22 @@
 //   K_m = floor(t_m - W/2) + 1   (window {k : -W/2 < k - t_m <= W/2}, R9)
 //
 // B200 design:
-//   * A persistent CTA owns tiles of M = T*R consecutive outputs of one pulse; the input span a
-//     tile needs (~M*beta + W + R samples) is staged into shared memory with cp.async (zero-
-//     filled outside [0, n)) one tile ahead, double-buffered, so HBM latency hides behind the
-//     previous tile's taps.  R = 9 is odd: lanes' windows start ~9 samples apart and land on
-//     distinct banks without padding, so window loads are plain base+immediate addresses.
-//   * A thread owns R consecutive outputs.  Their windows slide by one sample per output
-//     except where the fractional position wraps; all R windows lie inside a union of W+1
-//     taps [B, B + W] relative to a per-output base B + r, so the thread streams the union
-//     once through a register window (one LDS per tap, reused by all R outputs) and masks
-//     the single edge tap each output does not own.  The complex x real MACs are FFMA2
-//     (packed f32x2, one issue slot per complex sample); results leave through shared memory
-//     as coalesced 16-byte stores.
+//   * A persistent CTA (8 warps, 2 per SM) owns tiles of M = 256 R consecutive outputs of one
+//     pulse.  The input span a tile needs (~M beta + W + R samples) is staged into shared memory by
+//     the TMA engine (2-D tensor map {n, pulses}, hardware zero fill outside [0, n): R12) one tile
+//     ahead into one of three buffers with full/empty mbarriers, so HBM latency hides behind the
+//     taps and warps drift up to a tile apart without a CTA barrier.
+//   * A thread owns R = 11 consecutive outputs (odd: lanes' windows start R samples apart and land
+//     on distinct banks).  Their windows slide by one sample per output except where the position
+//     wraps; all R windows lie inside a union of W + 1 taps, streamed once through a register window
+//     (one LDS per tap, reused by all R outputs); each output masks the one edge tap it does not own.
+//     The complex x real MACs are FFMA2 (packed f32x2).  Each warp's 32 R contiguous outputs leave
+//     as one bulk async copy (shared -> global) issued by lane 0.
 //   * Taps are evaluated on the fly in FP32 (no LUT; LUT quantisation breaks 1e-5 parity):
 //     per thread, per tap, w = sinc(v - jj) and w' = sinc'(v - jj) at the thread's reference
 //     position v (exact binary64 position, reduced to [-1/2, 1/2] before the FP32 cast so
 //     the centre tap keeps full relative precision); each output then uses
 //     h = w + w' delta_r (+ w''/2 delta_r^2), delta_r = (r - r_ref)(beta - 1) exactly.
-//     With |delta| <= 2e-3 the truncation error is < 2e-9 (second order), far inside 1e-5.
 //   * The slow path (|beta - 1| too large for the union/Taylor scheme) evaluates every
 //     output directly (Alg. 1 structure).
 #include "doppler_tile.cuh"
@@ -32,8 +30,11 @@
 
 namespace dc {
 
-// Persistent, double-buffered pipeline: while the CTA computes tile i from one shared buffer,
-// the input span of tile i + gridDim.x streams into the other with cp.async (zero-filled).
+// Persistent pipeline over kDopBufs input buffers: thread 0 (the producer) stages tile i + 1 with the
+// TMA engine while the CTA computes tile i; each buffer has a `full` transaction mbarrier (TMA bytes)
+// and an `empty` mbarrier (one arrival per consumer warp once its lanes have read the buffer), so warps
+// run up to one tile apart with no CTA-wide barrier.  The producer writes the tile geometry next to the
+// buffer before its arrive (release), consumers read it after their wait (acquire).
 // WT > 0: the tap count W is a compile-time constant (fully unrolled tap loop); WT = 0: runtime W.
 #ifndef DC_DOP_MINB
 #define DC_DOP_MINB 2
@@ -45,43 +46,45 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
                         int buf_elems, const __grid_constant__ TaperCoef tc) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   extern __shared__ __align__(1024) float4 xs4[];
-  float2 *xs = reinterpret_cast<float2 *>(xs4);
-  float2 *ob = xs + 2 * buf_elems;  // output staging for coalesced stores
-  uint64_t *bars = reinterpret_cast<uint64_t *>(ob + kDopM);  // one mbarrier per staging buffer
+  float2 *xs = reinterpret_cast<float2 *>(xs4);                     // kDopBufs x buf_elems input spans
+  float2 *ob = xs + kDopBufs * buf_elems;                            // kDopM output staging (per warp)
+  DopTile *tiles = reinterpret_cast<DopTile *>(ob + kDopM);          // geometry of the tile in each buffer
+  uint64_t *full = reinterpret_cast<uint64_t *>(tiles + kDopBufs);   // TMA completion per buffer
+  uint64_t *empty = full + kDopBufs;                                 // consumer-warp release per buffer
   const int W = (WT > 0) ? WT : W_rt;
-  const int tid = threadIdx.x;
-  const int64_t tiles_per_pulse = (n + kDopM - 1) / kDopM;
-  const int64_t total = pulses * tiles_per_pulse;
-  const double halfW = 0.5 * (double)W;
-  int64_t item = blockIdx.x;
-  if (item >= total) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t tiles_per_pulse = (uint32_t)((n + kDopM - 1) / kDopM);
+  const uint32_t total = (uint32_t)pulses * tiles_per_pulse;
+  if (blockIdx.x >= total) return;
+  const uint32_t my_tiles = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  auto produce = [&](uint32_t i) {  // thread 0: stage local tile i into buffer i % kDopBufs
+    const int b = (int)(i % kDopBufs);
+    if (i >= (uint32_t)kDopBufs) mbar_wait(&empty[b], ((i / kDopBufs) - 1) & 1u);  // tile i - kDopBufs released
+    const uint32_t it = blockIdx.x + i * gridDim.x;
+    const DopTile t = dop_tile(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
+    tiles[b] = t;  // published to the consumers by the arrive below (release) / their wait (acquire)
+    dop_stage_tma(xs + b * buf_elems, t, &xmap, &full[b]);
+  };
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int b = 0; b < kDopBufs; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kDopT / 32);
+    }
     mbar_fence_init();
+    produce(0);
   }
   __syncthreads();
-  DopTile cur = dop_tile(item, tiles_per_pulse, W, pp, pulse_base);
-  if (tid == 0) dop_stage_tma(xs, cur, &xmap, &bars[0]);
-  int bsel = 0;
-  unsigned phase[2] = {0u, 0u};
-  for (; item < total; item += gridDim.x) {
-    // ---- prefetch the next tile into the other buffer (its readers finished at the last barrier)
-    const int64_t nitem = item + gridDim.x;
-    DopTile nxt;
-    if (nitem < total) {
-      nxt = dop_tile(nitem, tiles_per_pulse, W, pp, pulse_base);
-      if (tid == 0) dop_stage_tma(xs + (bsel ^ 1) * buf_elems, nxt, &xmap, &bars[bsel ^ 1]);
-    }
-    mbar_wait(&bars[bsel], phase[bsel]);
-    phase[bsel] ^= 1u;
-    const float2 *sb = xs + bsel * buf_elems;
-
-    dop_tile_compute<SECOND, WT, 0, TAPER>(sb, cur, W, ob, y, n, carrier, &tc);
-    __syncthreads();  // output staging and input buffer bsel free for reuse
-    cur = nxt;
-    bsel ^= 1;
+  float2 *obw = ob + (tid >> 5) * kDopSeg;
+  for (uint32_t i = 0; i < my_tiles; ++i) {
+    if (tid == 0 && i + 1 < my_tiles) produce(i + 1);
+    const int b = (int)(i % kDopBufs);
+    mbar_wait(&full[b], (i / kDopBufs) & 1u);
+    const DopTile cur = tiles[b];
+    dop_tile_compute<SECOND, WT, TAPER>(xs + b * buf_elems, cur, W, obw, y, n, carrier, &tc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done reading buffer b
   }
+  if (lane == 0) bulk_store_wait_all();  // the warp's last output segment has left shared memory
 }
 
 // Exact-tap, one-output-per-thread path (Alg. 1 structure) for any alpha.
@@ -141,7 +144,7 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
   const int span = (int)(kDopM * (1.0 + kDopMaxDrift)) + a.taps + kDopR + 16;
   const int buf = (span + kDopBox - 1) / kDopBox * kDopBox;  // whole TMA boxes
-  const size_t smem = sizeof(float2) * (2 * (size_t)buf + kDopM) + 2 * sizeof(uint64_t) + 1024;
+  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + kDopM) + kDopBufs * (sizeof(DopTile) + 2 * sizeof(uint64_t)) + 1024;
   CUtensorMap xmap;
   {
     const uint64_t dims[2] = {(uint64_t)a.n, (uint64_t)a.pulses};

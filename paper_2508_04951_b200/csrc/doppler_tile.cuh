@@ -1,5 +1,5 @@
-// doppler_tile.cuh -- Doppler (windowed sinc) tile machinery shared by the doppler kernels
-// and the fused persistent correction kernel.  See doppler_kernel.cu for the method notes.
+// doppler_tile.cuh -- Doppler (windowed sinc) tile machinery of doppler_pipe_kernel.
+// See doppler_kernel.cu for the method notes (Eq. 16; window P:L533; readings R8-R12).
 #pragma once
 #include <algorithm>
 #include <type_traits>
@@ -9,13 +9,19 @@
 
 namespace dc {
 
-constexpr int kDopT = 256;  // threads per CTA
+constexpr int kDopT = 256;  // threads per CTA (8 consumer warps)
 #ifndef DC_DOP_R
 #define DC_DOP_R 11
 #endif
 constexpr int kDopR = DC_DOP_R;  // outputs per thread: odd, so lanes' windows (R samples apart) hit distinct banks
 constexpr int kDopM = kDopT * kDopR;     // outputs per tile
+constexpr int kDopSeg = 32 * kDopR;      // outputs per warp (even: 16-byte aligned bulk stores)
 constexpr double kDopMaxDrift = 2.0e-3;  // max |beta - 1| * R / 2 for the fast path
+#ifndef DC_DOP_NBUF
+#define DC_DOP_NBUF 3
+#endif
+constexpr int kDopBufs = DC_DOP_NBUF;    // input staging buffers (prefetch distance 1: warps may lag one tile)
+static_assert(kDopSeg % 2 == 0, "warp segments must be 16-byte multiples");
 
 __device__ __forceinline__ float frcp(float x) {
   float r;
@@ -23,28 +29,23 @@ __device__ __forceinline__ float frcp(float x) {
   return r;
 }
 
-// async 8-byte global -> shared copy with zero fill when `valid` is false (cp.async, LDGSTS)
-__device__ __forceinline__ void cp_async8(float2 *smem_dst, const float2 *gsrc, bool valid) {
-  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem_dst);
-  const int src_size = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(src_size) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
+// Geometry of one tile (pulse, first output m0, staged span [Bcta, Bcta + span), beta): computed
+// by the producer thread when it stages the tile and kept in shared memory next to the buffer.
 struct DopTile {
   int64_t pulse, m0, Bcta;
   double beta;
-  int span;
+  int span, pad;
 };
 
-__device__ __forceinline__ DopTile dop_tile(int64_t item, int64_t tiles_per_pulse, int W,
-                                            const PulseParams *__restrict__ pp, int64_t pulse_base) {
+// tile `item` = (pulse, tile of kDopM outputs) -- 32-bit index arithmetic (items < 2^32: pulses per
+// launch <= 65535, tiles per pulse <= 2^24 / kDopM); beta = that pulse's 1/alpha
+__device__ __forceinline__ uint32_t dop_pulse(uint32_t item, uint32_t tiles_per_pulse) { return item / tiles_per_pulse; }
+__device__ __forceinline__ DopTile dop_tile(uint32_t item, uint32_t tiles_per_pulse, int W, double beta) {
   DopTile t;
-  t.pulse = item / tiles_per_pulse;
-  t.m0 = (item - t.pulse * tiles_per_pulse) * kDopM;
-  t.beta = pp[pulse_base + t.pulse].beta;
+  const uint32_t pulse = item / tiles_per_pulse;
+  t.pulse = pulse;
+  t.m0 = (int64_t)(item - pulse * tiles_per_pulse) * kDopM;
+  t.beta = beta;
   const double halfW = 0.5 * (double)W;
   const int lo_shift = (t.beta < 1.0) ? 1 : 0;
   t.Bcta = (int64_t)floor((double)t.m0 * t.beta - halfW) + 1 - lo_shift;
@@ -52,6 +53,7 @@ __device__ __forceinline__ DopTile dop_tile(int64_t item, int64_t tiles_per_puls
   const int64_t mlast = t.m0 + kDopM - 1;
   const int64_t Kend = (int64_t)floor((double)mlast * t.beta - halfW) + 1 + W + kDopR + 4;
   t.span = (int)(Kend - t.Bcta);
+  t.pad = 0;
   return t;
 }
 
@@ -65,18 +67,6 @@ __device__ __forceinline__ void dop_stage_tma(float2 *buf, const DopTile &t, con
   fence_proxy_async();
   mbar_arrive_expect_tx(bar, (unsigned)(nb * kDopBox * sizeof(float2)));
   for (int i = 0; i < nb; ++i) tma_load_2d(buf + i * kDopBox, xmap, (int)(t.Bcta + i * kDopBox), (int)t.pulse, bar);
-}
-
-// sinc weight w = sinc(d), w1 = sinc'(d), w2 = sinc''(d) at d = u - m (u in [-1/2, 1/2]):
-// sin(pi d) = (-1)^m sin(pi u), cos(pi d) = (-1)^m cos(pi u); S = sin(pi u)/pi, Cc = cos(pi u).
-template <bool SECOND>
-__device__ __forceinline__ void tap_w(float u, int m, float S, float Cc, float &w, float &w1, float &w2) {
-  const float d = u - (float)m;
-  const float inv = frcp(d);
-  const float s = (m & 1) ? -S : S, c = (m & 1) ? -Cc : Cc;
-  w = s * inv;
-  w1 = inv * (c - w);
-  w2 = SECOND ? fmaf(-9.8696044010893586f, w, -2.f * w1 * inv) : 0.f;
 }
 
 // Kaiser taper K(d) and K'(d) (reading R17) by Horner on the normalised I0 series in
@@ -95,45 +85,60 @@ __device__ __forceinline__ void kaiser_taper(const TaperCoef &tc, float d, float
   dK = db * (-2.0f * tc.qa * tc.inv_L2 * d);  // dP/dq * dq/dd
 }
 
-// One doppler tile: R = 9 outputs per thread from the staged span sb (x[Bcta + i] = sb[i]),
-// carrier rotation, then a coalesced store of the tile's M outputs through `ob` (one barrier
-// inside; callers add the trailing barrier before ob / sb are reused).
-// BAR = 0: the whole CTA (kDopT threads) computes the tile; BAR > 0: named barrier BAR over the
-// kDopT threads 0 .. kDopT-1 (the consumer warps of a warp-specialised kernel).
+// Window membership of the thread's R outputs (reading R9, the oracle's roundings): output r owns the
+// union taps [a_r, a_r + W - 1], a_r in {0, 1}, a_r = 1 iff its window start K_r = floor(x_r) + 1
+// equals B + r + 1, i.e. iff x_r = fl(fl((mt + r) beta) - W/2) >= B + r (exact binary64 comparison:
+// integers below 2^53).  X_r = x_r - (B + r) moves linearly in r by beta - 1 up to ~1 ulp(t) of
+// rounding, so when the first and last outputs are on the same side by a clear margin all R decisions
+// agree; only a thread whose outputs straddle a window step (~R |beta - 1| of all threads) evaluates
+// each output.  Returns the bit set {r : a_r = 1}.
+__device__ __forceinline__ uint32_t dop_membership(double md, double beta, double halfW, double Bd, double x0) {
+  constexpr uint32_t kAll = (1u << kDopR) - 1u;
+  constexpr double kMargin = 1.0e-7;  // >> rounding of t (ulp(2^25) = 7.5e-9)
+  const double X0 = x0 - Bd;          // exact (Sterbenz: |x0 - Bd| <= 1)
+  const double XL = __dsub_rn(__dmul_rn(md + (double)(kDopR - 1), beta), halfW) - (Bd + (double)(kDopR - 1));
+  if (X0 >= kMargin && XL >= kMargin) return kAll;
+  if (X0 <= -kMargin && XL <= -kMargin) return 0u;
+  uint32_t own1 = 0;
+#pragma unroll 1
+  for (int r = 0; r < kDopR; ++r)
+    own1 |= (__dsub_rn(__dmul_rn(md + (double)r, beta), halfW) >= Bd + (double)r) ? (1u << r) : 0u;
+  return own1;
+}
+
+// One doppler tile: R outputs per thread from the staged span sb (x[Bcta + i] = sb[i]), carrier
+// rotation, then the warp's R x 32 contiguous outputs leave through its shared-memory segment `ob`
+// (kDopSeg samples) as ONE bulk async copy issued by lane 0 (no LDS/STG per output, no CTA barrier).
 // TAPER > 0: Kaiser-tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only), with
 // TAPER series terms.
-template <bool SECOND, int WT, int BAR = 0, int TAPER = 0>
+template <bool SECOND, int WT, int TAPER = 0>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
                                                  double carrier, const TaperCoef *tcp = nullptr) {
   static_assert(!(TAPER > 0 && SECOND), "the tapered path is first order");
   const int W = (WT > 0) ? WT : W_rt;
   const double halfW = 0.5 * (double)W;
-  const int tid = threadIdx.x;
-    // ---- this thread's R consecutive outputs: exact binary64 window bookkeeping
+  const int tid = threadIdx.x, lane = tid & 31;
+  // ---- this thread's R consecutive outputs: exact binary64 window bookkeeping.  Window decisions
+  // use the oracle's two separately rounded binary64 operations fl(fl(m beta) - W/2) (__dmul_rn /
+  // __dsub_rn: never contracted into an FMA), so membership matches R9 exactly.
   const int64_t mt = cur.m0 + (int64_t)tid * kDopR;
   const double beta = cur.beta;
   const int lo_shift = (beta < 1.0) ? 1 : 0;
-  // window decisions use the oracle's two separately rounded binary64 operations, fl(fl(m beta) - W/2)
-  // (__dmul_rn / __dsub_rn: never contracted into an FMA), so membership matches R9 exactly
-  const int64_t B = (int64_t)floor(__dsub_rn(__dmul_rn((double)mt, beta), halfW)) + 1 - lo_shift;
-  float mask0[kDopR], maskW[kDopR];
-#pragma unroll
-  for (int r = 0; r < kDopR; ++r) {
-    const int64_t Kr = (int64_t)floor(__dsub_rn(__dmul_rn((double)(mt + r), beta), halfW)) + 1;
-    const int a = (int)(Kr - r - B);  // 0 or 1: this output's window offset inside the union
-    mask0[r] = (a == 0) ? 1.f : 0.f;
-    maskW[r] = (a == 1) ? 1.f : 0.f;
-  }
-  // Taylor steps delta_r = (r - R/2)(beta - 1): pairs for FFMA2 + one single
+  const double md = (double)mt;
+  const double x0 = __dsub_rn(__dmul_rn(md, beta), halfW);
+  const int64_t B = (int64_t)floor(x0) + 1 - lo_shift;  // union base: x[B + i], i = 0 .. W + R - 1
+  const double Bd = (double)B;
+  const uint32_t own1 = dop_membership(md, beta, halfW, Bd, x0);
+  // Taylor steps delta_r = (r - R/2)(beta - 1): pairs for FFMA2 (+ one single for odd R)
   constexpr int RC = kDopR / 2;  // reference output
   const float db = (float)(beta - 1.0);
   float2 dl[kDopR / 2];
 #pragma unroll
   for (int h = 0; h < kDopR / 2; ++h) dl[h] = make_float2((2 * h - RC) * db, (2 * h + 1 - RC) * db);
-  const float dlast = (kDopR - 1 - RC) * db;
+  const float dlast = (kDopR - 1 - RC) * db;  // the unpaired last output (odd R)
   // reference position inside the union, split into nearest integer + fraction in [-1/2, 1/2]
-  const double vref = (double)(mt + RC) * beta - (double)(B + RC);
+  const double vref = (md + (double)RC) * beta - (Bd + (double)RC);
   const double ic_d = rint(vref);
   const int ic = (int)ic_d;
   const float u = __double2float_rn(vref - ic_d);
@@ -160,12 +165,17 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   const float2 *xb = sb + (B - cur.Bcta);  // x[B + i] = xb[i]
   // sign of tap jj: (-1)^(jj - ic); fold (-1)^ic into the per-thread constants
   const float Sp = (ic & 1) ? -S : S, Cp = (ic & 1) ? -Cc : Cc;
+  // distance of union tap jj from the reference position: d = u - (jj - ic), the integer part exact
+  // and one rounding (a running d -= 1 from u + ic would lose u's low bits near the centre tap)
   const float icf = (float)ic;
   float2 acc[kDopR];
 #pragma unroll
   for (int r = 0; r < kDopR; ++r) acc[r] = make_float2(0.f, 0.f);
 
-  auto mac = [&](const float2 *xv, float w, float w1, float w2, const float *mask) {
+  // EDGE = 0: interior tap (all R outputs); 1: union tap 0 (outputs with a_r = 0); 2: union tap W (a_r = 1)
+  auto mac = [&](const float2 *xv, float w, float w1, float w2, auto EDGEc) {
+    constexpr int EDGE = decltype(EDGEc)::value;
+    auto keep = [&](int r) { return EDGE == 0 || (((own1 >> r) & 1u) == (EDGE == 2 ? 1u : 0u)); };
 #pragma unroll
     for (int h = 0; h < kDopR / 2; ++h) {
       float2 hh;
@@ -175,23 +185,24 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       } else {
         hh = __ffma2_rn(make_float2(w1, w1), dl[h], make_float2(w, w));
       }
-      if (mask) {
-        hh.x *= mask[2 * h];
-        hh.y *= mask[2 * h + 1];
+      if (EDGE) {
+        hh.x = keep(2 * h) ? hh.x : 0.f;
+        hh.y = keep(2 * h + 1) ? hh.y : 0.f;
       }
       acc[2 * h] = __ffma2_rn(xv[2 * h], make_float2(hh.x, hh.x), acc[2 * h]);
       acc[2 * h + 1] = __ffma2_rn(xv[2 * h + 1], make_float2(hh.y, hh.y), acc[2 * h + 1]);
     }
-    float hl = SECOND ? fmaf(fmaf(0.5f * w2, dlast, w1), dlast, w) : fmaf(w1, dlast, w);
-    if (mask) hl *= mask[kDopR - 1];
-    acc[kDopR - 1] = __ffma2_rn(xv[kDopR - 1], make_float2(hl, hl), acc[kDopR - 1]);
+    if constexpr (kDopR & 1) {
+      float hl = SECOND ? fmaf(fmaf(0.5f * w2, dlast, w1), dlast, w) : fmaf(w1, dlast, w);
+      if (EDGE) hl = keep(kDopR - 1) ? hl : 0.f;
+      acc[kDopR - 1] = __ffma2_rn(xv[kDopR - 1], make_float2(hl, hl), acc[kDopR - 1]);
+    }
   };
-  // weights of union tap jj: d = u - (jj - ic) (exact integer subtraction, then one rounding);
+  // weights of union tap jj at distance d = u - (jj - ic):
   // sinc = (-1)^(jj-ic) S / d, sinc' = ((-1)^(jj-ic) C - sinc) / d, sinc'' = -pi^2 sinc - 2 sinc'/d.
   // TINY: override the centre tap (jj == ic) with its series values.
-  auto weights = [&](int jj, auto TINYc, float &w, float &w1, float &w2) {
+  auto weights = [&](int jj, float d, auto TINYc, float &w, float &w1, float &w2) {
     constexpr bool TINY = decltype(TINYc)::value;
-    const float d = u - ((float)jj - icf);
     const float inv = frcp(d);
     const float s = (jj & 1) ? -Sp : Sp, c = (jj & 1) ? -Cp : Cp;
     w = s * inv;
@@ -217,17 +228,19 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
 #pragma unroll
     for (int r = 0; r < kDopR; ++r) xw[r] = xb[r];
     {
+      const float d = u + icf;
       float w, w1, w2;
-      weights(0, TINYc, w, w1, w2);
-      mac(xw, w, w1, w2, mask0);
+      weights(0, d, TINYc, w, w1, w2);
+      mac(xw, w, w1, w2, std::integral_constant<int, 1>());
     }
     auto step = [&](int jj) {  // slide the window to tap jj and apply it (interior taps)
 #pragma unroll
       for (int r = 0; r < kDopR - 1; ++r) xw[r] = xw[r + 1];
       xw[kDopR - 1] = xb[jj + kDopR - 1];
+      const float d = u - ((float)jj - icf);
       float w, w1, w2;
-      weights(jj, TINYc, w, w1, w2);
-      mac(xw, w, w1, w2, nullptr);
+      weights(jj, d, TINYc, w, w1, w2);
+      mac(xw, w, w1, w2, std::integral_constant<int, 0>());
     };
     if constexpr (WT > 0) {
 #pragma unroll
@@ -240,9 +253,10 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
 #pragma unroll
       for (int r = 0; r < kDopR - 1; ++r) xw[r] = xw[r + 1];
       xw[kDopR - 1] = xb[W + kDopR - 1];
+      const float d = u - ((float)W - icf);
       float w, w1, w2;
-      weights(W, TINYc, w, w1, w2);
-      mac(xw, w, w1, w2, maskW);
+      weights(W, d, TINYc, w, w1, w2);
+      mac(xw, w, w1, w2, std::integral_constant<int, 2>());
     }
   };
   if (tiny) {
@@ -251,7 +265,7 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
     taps(std::false_type());
   }
 
-  // ---- carrier rotation (reading R10), then coalesced store through shared memory
+  // ---- carrier rotation (reading R10)
   const double g = carrier * (1.0 - beta);
   if (g != 0.0) {
 #pragma unroll
@@ -260,24 +274,20 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       acc[r] = cmul(acc[r], expm2pi(__double2float_rn(psi - rint(psi))));
     }
   }
-  // a warp's 32 x R outputs are contiguous (thread t owns outputs [t R, t R + R)): each warp stages
-  // its own segment and stores it with coalesced 16-byte stores -- no CTA barrier (BAR unused)
-#pragma unroll
-  for (int r = 0; r < kDopR; ++r) ob[tid * kDopR + r] = acc[r];
+  // ---- store: the warp's 32 x R outputs are contiguous (thread t owns [t R, t R + R)).  Lane 0's
+  // previous bulk store must have finished reading the segment before it is overwritten.
+  if (lane == 0) bulk_store_wait_read();
   __syncwarp();
-  {
-    constexpr int kSeg = 32 * kDopR;  // outputs per warp (even: 16-byte aligned segments)
-    const int w = tid >> 5, lane = tid & 31;
-    const int64_t mw = cur.m0 + (int64_t)w * kSeg;
-    float2 *yp = y + cur.pulse * n + mw;
-    const float2 *os = ob + w * kSeg;
-    const int64_t valid = min((int64_t)kSeg, n - mw);
-    if (valid == kSeg) {
-      const float4 *o4 = reinterpret_cast<const float4 *>(os);
-      float4 *y4 = reinterpret_cast<float4 *>(yp);
-      for (int i = lane; i < kSeg / 2; i += 32) __stcs(y4 + i, o4[i]);
-    } else {
-      for (int i = lane; i < valid; i += 32) yp[i] = os[i];
+#pragma unroll
+  for (int r = 0; r < kDopR; ++r) ob[lane * kDopR + r] = acc[r];
+  fence_proxy_async();  // generic-proxy writes -> visible to the bulk copy (async proxy)
+  __syncwarp();
+  if (lane == 0) {
+    const int64_t mw = cur.m0 + (int64_t)(tid >> 5) * kDopSeg;
+    const int64_t valid = min((int64_t)kDopSeg, n - mw);  // even: n and mw are even
+    if (valid > 0) {
+      bulk_store(y + cur.pulse * n + mw, ob, (unsigned)(valid * sizeof(float2)));
+      bulk_commit();
     }
   }
 }

@@ -106,4 +106,18 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
                : "memory");
 }
 
+// 1-D bulk copy shared -> global (contiguous bytes, multiple of 16, both 16-byte aligned), tracked by
+// the issuing thread's bulk async-group; the shared source may be rewritten once
+// bulk_store_wait_read() returns
+__device__ __forceinline__ void bulk_store(void *gdst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// all of this thread's committed bulk stores have finished READING shared memory
+__device__ __forceinline__ void bulk_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// ... and their writes are complete (before the CTA exits)
+__device__ __forceinline__ void bulk_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 }  // namespace dc
