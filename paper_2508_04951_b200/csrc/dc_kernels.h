@@ -93,7 +93,10 @@ struct DopplerArgs {
   bool taper;       // Kaiser taper on (coefficients in tc)
   TaperCoef tc;
   int taper_terms;  // series terms needed (17 or kTaperTerms)
+  void *desc;       // plan-owned per-CTA tile-geometry slots (kDopDescBytes)
 };
+constexpr int kDopMaxCtas = 1024;                       // persistent Doppler grid cap
+constexpr size_t kDopDescBytes = (size_t)kDopMaxCtas * 4 * 48;
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
 int doppler_path(double max_abs_beta_m1, bool taper = false);
 

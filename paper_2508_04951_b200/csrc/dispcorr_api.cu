@@ -106,6 +106,7 @@ struct dc_plan_s {
   int taper_terms = dc::kTaperTerms;
   bool ref_set = false;
   float2 *scratch = nullptr;  // launch-group buffer of dc_correct: chunk * n samples
+  void *dop_desc = nullptr;   // Doppler kernel: per-CTA tile-geometry slots (dc::kDopDescBytes)
   int64_t scratch_bytes = 0;
   cudaEvent_t ev_stream = nullptr;  // dc_set_stream: orders the new stream after the old one
   // host-path buffers (lazily allocated)
@@ -401,7 +402,8 @@ bool compress_supported(const dc_plan_s *p) {
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                       int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
-  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, ln.cap, p->taper, p->tc, p->taper_terms};
+  dc::DopplerArgs a{src, dst, pulses, p->n, p->taps, pp, pulse_base, p->fc / p->fs, ln.st, ln.cap, p->taper, p->tc, p->taper_terms,
+                    p->dop_desc};
   ProfScope ps(p, DC_K_DOPPLER, pulses * p->n, ln.st);
   DC_CUDA(dc::launch_doppler(a, max_abs_beta_m1), "doppler kernel launch");
   return DC_OK;
@@ -588,6 +590,10 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
       return cleanup(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
   if (cudaEventCreateWithFlags(&p->ev_stream, cudaEventDisableTiming) != cudaSuccess)
     return cleanup(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
+  if (cudaMalloc(&p->dop_desc, dc::kDopDescBytes) != cudaSuccess) {
+    cudaGetLastError();
+    return cleanup(fail(DC_ERR_OUT_OF_MEMORY, "Doppler tile-geometry slots"));
+  }
   *out = p;
   return DC_OK;
 }
@@ -609,6 +615,7 @@ dc_status dc_plan_destroy(dc_plan_t p) {
     if (s.dev_raw) cudaFree(s.dev_raw);
   }
   if (p->ev_stream) cudaEventDestroy(p->ev_stream);
+  if (p->dop_desc) cudaFree(p->dop_desc);
   for (int i = 0; i < 2; ++i) {
     if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
     if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);

@@ -33,8 +33,8 @@ namespace dc {
 // Persistent pipeline over kDopBufs input buffers: thread 0 (the producer) stages tile i + 1 with the
 // TMA engine while the CTA computes tile i; each buffer has a `full` transaction mbarrier (TMA bytes)
 // and an `empty` mbarrier (one arrival per consumer warp once its lanes have read the buffer), so warps
-// run up to one tile apart with no CTA-wide barrier.  The producer writes the tile geometry next to the
-// buffer before its arrive (release), consumers read it after their wait (acquire).
+// run up to one tile apart with no CTA-wide barrier.  The tile geometry reaches the consumers through the
+// TMA engine too (from a per-CTA global slot), counted by the same `full` barrier as the data.
 // WT > 0: the tap count W is a compile-time constant (fully unrolled tap loop); WT = 0: runtime W.
 #ifndef DC_DOP_MINB
 #define DC_DOP_MINB 2
@@ -43,13 +43,16 @@ template <bool SECOND, int WT, int TAPER>
 __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
-                        int buf_elems, const __grid_constant__ TaperCoef tc) {
+                        int buf_elems, const __grid_constant__ TaperCoef tc, DopTile *__restrict__ gdesc,
+                        const __grid_constant__ CUtensorMap dmap) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);                     // kDopBufs x buf_elems input spans
   float2 *ob = xs + kDopBufs * buf_elems;                            // kDopM output staging (per warp)
-  DopTile *tiles = reinterpret_cast<DopTile *>(ob + kDopM);          // geometry of the tile in each buffer
-  uint64_t *full = reinterpret_cast<uint64_t *>(tiles + kDopBufs);   // TMA completion per buffer
+  // geometry of the tile in each buffer: 128-byte slots (TMA destinations are 128-byte aligned)
+  DopTile *tiles = reinterpret_cast<DopTile *>(ob + kDopM);
+  auto dslot = [&](int b) { return reinterpret_cast<DopTile *>(reinterpret_cast<char *>(tiles) + 128 * b); };
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(tiles) + 128 * kDopBufs);  // TMA completion
   uint64_t *empty = full + kDopBufs;                                 // consumer-warp release per buffer
   const int W = (WT > 0) ? WT : W_rt;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -62,8 +65,8 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     if (i >= (uint32_t)kDopBufs) mbar_wait(&empty[b], ((i / kDopBufs) - 1) & 1u);  // tile i - kDopBufs released
     const uint32_t it = blockIdx.x + i * gridDim.x;
     const DopTile t = dop_tile(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
-    tiles[b] = t;  // published to the consumers by the arrive below (release) / their wait (acquire)
-    dop_stage_tma(xs + b * buf_elems, t, &xmap, &full[b]);
+    const int slot = (int)blockIdx.x * kDopBufs + b;
+    dop_stage_tma(xs + b * buf_elems, t, &xmap, &full[b], dslot(b), gdesc + slot, &dmap, slot);
   };
   if (tid == 0) {
     for (int b = 0; b < kDopBufs; ++b) {
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     if (tid == 0 && i + 1 < my_tiles) produce(i + 1);
     const int b = (int)(i % kDopBufs);
     mbar_wait(&full[b], (i / kDopBufs) & 1u);
-    const DopTile cur = tiles[b];
+    const DopTile cur = *dslot(b);
     dop_tile_compute<SECOND, WT, TAPER>(xs + b * buf_elems, cur, W, obw, y, n, carrier, &tc);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done reading buffer b
@@ -144,7 +147,7 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
   const int span = (int)(kDopM * (1.0 + kDopMaxDrift)) + a.taps + kDopR + 16;
   const int buf = (span + kDopBox - 1) / kDopBox * kDopBox;  // whole TMA boxes
-  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + kDopM) + kDopBufs * (sizeof(DopTile) + 2 * sizeof(uint64_t)) + 1024;
+  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + kDopM) + kDopBufs * (128 + 2 * sizeof(uint64_t)) + 1024;
   CUtensorMap xmap;
   {
     const uint64_t dims[2] = {(uint64_t)a.n, (uint64_t)a.pulses};
@@ -161,8 +164,17 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDopT, smem);
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
+  grid = std::min<int64_t>(grid, kDopMaxCtas);
+  static_assert(kDopBufs <= 4 && sizeof(DopTile) == 48, "kDopDescBytes sizing");
+  CUtensorMap dmap;  // the per-CTA geometry slots: {6 x 8 bytes, slot}, one 48-byte box per tile
+  {
+    const uint64_t dims[2] = {6, (uint64_t)kDopMaxCtas * 4};
+    const uint64_t strides[1] = {sizeof(DopTile)};
+    const uint32_t box[2] = {6u, 1u};
+    if (!encode_tile_map(&dmap, a.desc, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  }
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kDopT), smem, a.stream, xmap, a.y, a.n, a.taps, a.pp, a.pulse_base,
-                    a.carrier_cycles_per_sample, a.pulses, buf, a.tc);
+                    a.carrier_cycles_per_sample, a.pulses, buf, a.tc, reinterpret_cast<DopTile *>(a.desc), dmap);
 }
 
 template <bool SECOND, int TAPER = 0>

@@ -31,11 +31,13 @@ __device__ __forceinline__ float frcp(float x) {
 
 // Geometry of one tile (pulse, first output m0, staged span [Bcta, Bcta + span), beta): computed
 // by the producer thread when it stages the tile and kept in shared memory next to the buffer.
-struct DopTile {
+struct __align__(16) DopTile {
   int64_t pulse, m0, Bcta;
   double beta;
-  int span, pad;
+  int span, pad0;
+  int64_t pad1;
 };
+static_assert(sizeof(DopTile) == 48, "bulk copies move multiples of 16 bytes");
 
 // tile `item` = (pulse, tile of kDopM outputs) -- 32-bit index arithmetic (items < 2^32: pulses per
 // launch <= 65535, tiles per pulse <= 2^24 / kDopM); beta = that pulse's 1/alpha
@@ -53,7 +55,8 @@ __device__ __forceinline__ DopTile dop_tile(uint32_t item, uint32_t tiles_per_pu
   const int64_t mlast = t.m0 + kDopM - 1;
   const int64_t Kend = (int64_t)floor((double)mlast * t.beta - halfW) + 1 + W + kDopR + 4;
   t.span = (int)(Kend - t.Bcta);
-  t.pad = 0;
+  t.pad0 = 0;
+  t.pad1 = 0;
   return t;
 }
 
@@ -62,10 +65,18 @@ __device__ __forceinline__ DopTile dop_tile(uint32_t item, uint32_t tiles_per_pu
 // (R12).  Issued by one thread; completion is the buffer's transaction-count mbarrier.
 constexpr int kDopBox = 256;
 __device__ __forceinline__ int dop_nbox(const DopTile &t) { return (t.span + kDopBox - 1) / kDopBox; }
-__device__ __forceinline__ void dop_stage_tma(float2 *buf, const DopTile &t, const CUtensorMap *xmap, uint64_t *bar) {
+// The tile's geometry travels with it: the producer writes it to its CTA's global slot and the TMA
+// engine lands it in `desc` (a 48-byte box of the tensor map dmap over the slots), counted by the same
+// mbarrier as the data -- consumers read it after their wait; no generic shared-memory write passes
+// between producer and consumers.
+__device__ __forceinline__ void dop_stage_tma(float2 *buf, const DopTile &t, const CUtensorMap *xmap, uint64_t *bar,
+                                              DopTile *desc, DopTile *gslot, const CUtensorMap *dmap, int slot) {
   const int nb = dop_nbox(t);
+  *gslot = t;
+  fence_proxy_async_global();  // the generic write above -> visible to the TMA read below
   fence_proxy_async();
-  mbar_arrive_expect_tx(bar, (unsigned)(nb * kDopBox * sizeof(float2)));
+  mbar_arrive_expect_tx(bar, (unsigned)(nb * kDopBox * sizeof(float2) + sizeof(DopTile)));
+  tma_load_2d(desc, dmap, 0, slot, bar);
   for (int i = 0; i < nb; ++i) tma_load_2d(buf + i * kDopBox, xmap, (int)(t.Bcta + i * kDopBox), (int)t.pulse, bar);
 }
 

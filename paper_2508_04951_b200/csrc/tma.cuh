@@ -106,6 +106,9 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned b
                : "memory");
 }
 
+// make this thread's generic-proxy global writes visible to its later async-proxy (bulk copy) reads
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+
 // 1-D bulk copy shared -> global (contiguous bytes, multiple of 16, both 16-byte aligned), tracked by
 // the issuing thread's bulk async-group; the shared source may be rewritten once
 // bulk_store_wait_read() returns

@@ -1,0 +1,35 @@
+"""compute-sanitizer tier (tier 4): memcheck, racecheck, synccheck and initcheck over one small
+launch of every libdispcorr kernel (tools/sanitize_driver.py) must report zero errors.  The kernels
+rely on TMA + transaction mbarriers, full/empty mbarrier pipelines, bulk async stores, cp.async and
+warp-private shared-memory exchanges; racecheck / synccheck check those hazards."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer_clean(tool):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not installed")
+    from paper_2508_04951_b200 import build
+    build.build()
+    r = subprocess.run([exe, "--tool", tool, "--print-limit", "10", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_driver.py")], cwd=ROOT, capture_output=True, text=True,
+                       timeout=1200)
+    out = r.stdout + r.stderr
+    assert "sanitize driver done" in out, out[-3000:]
+    summary = [ln for ln in out.splitlines() if "ERROR SUMMARY" in ln or "RACECHECK SUMMARY" in ln]
+    assert summary, out[-3000:]
+    m = re.search(r"(\d+) errors", summary[-1])
+    assert m and int(m.group(1)) == 0, "\n".join(summary) + "\n" + out[-3000:]
