@@ -85,14 +85,8 @@ static __device__ __noinline__ float phase_frac_exact(double k2, double fc, doub
   return __double2float_rn(nu - rint(nu));
 }
 
-// phase cycles of bin k of an n-point pulse with table entry g = 1/f_k (FP32 pair): the FP32-pair
-// product, or the exact binary64 path for huge |nu| (signed bin index: the Nyquist bin is negative, R2)
-__device__ __forceinline__ float phase_cycles(const PulseParams &pr, float2 g, long long k, long long n, double fc,
-                                              double fs_over_n) {
-  float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
-  if (fabsf(pr.nu_hi * g.x) >= kPhaseExactCycles) rf = phase_frac_exact(pr.k2, fc, fs_over_n, k >= n / 2 ? k - n : k);
-  return rf;
-}
+// the FP32-pair path is exact enough for this bin unless |nu| ~ |nu_hi g_hi| reaches kPhaseExactCycles
+__device__ __forceinline__ bool phase_needs_exact(float nu_hi, float2 g) { return fabsf(nu_hi * g.x) >= kPhaseExactCycles; }
 
 // ----------------------------------------------------------------------------- complex float
 // sm_100a has packed f32x2 FADD2/FMUL2/FFMA2: one issue slot per complex add / half a complex

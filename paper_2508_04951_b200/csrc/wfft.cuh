@@ -49,6 +49,36 @@ __device__ __forceinline__ float2 twn(uint32_t m, int log2n) {
   return make_float2(cs, -sn);
 }
 
+// Rare path of the Eq. 15 phase (bins with |nu| >= kPhaseExactCycles, i.e. within ~1 MHz of DC at
+// 100-200 TECU): bit s of `ex` marks element lane + 32 s of this lane, which the main loop rotated by
+// the FP32-pair phase; it is re-rotated by (exact binary64 phase - FP32-pair phase).  The warp's
+// samples go through its exchange buffer (each lane touches only its own slots) so that the
+// out-of-line binary64 routine is called from a loop with no sample registers live -- 32 inline
+// call sites in the phase loop cost the row pass 2.4x (measured, round 2).
+template <bool DISTORT, class KB>
+__device__ __forceinline__ void phase_exact_fixup(float2 (&v)[32], uint32_t ex, float2 *__restrict__ wk, int lane,
+                                                  const PulseParams &pr, const float2 *grow, KB kb_of, long long n,
+                                                  double fc, double fs_over_n) {
+  if (!__any_sync(0xffffffffu, ex != 0u)) return;
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < 32; ++s) wk[wpad(lane + 32 * s)] = v[s];
+#pragma unroll 1
+  while (ex != 0u) {
+    const int s = __ffs(ex) - 1;
+    ex &= ex - 1u;
+    const float2 g = grow[lane + 32 * s];
+    const long long k = kb_of(s);
+    float d = phase_frac_exact(pr.k2, fc, fs_over_n, k >= n / 2 ? k - n : k) - phase_frac(pr.nu_hi, pr.nu_lo, g);
+    d -= rintf(d);
+    float2 &e = wk[wpad(lane + 32 * s)];
+    e = cmul(e, expm2pi(DISTORT ? -d : d));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < 32; ++s) v[s] = wk[wpad(lane + 32 * s)];
+}
+
 struct WarpArgs {
   const float2 *src;
   float2 *dst;
@@ -190,15 +220,23 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
           for (int s = 0; s < 32; ++s) rc[s] = __ldg(a.ref + (int64_t)k1 * 1024 + lane + 32 * s);
         }
 #pragma unroll
+        uint32_t ex = 0u;  // elements needing the exact binary64 phase (phase_exact_fixup)
+#pragma unroll
         for (int s = 0; s < 32; ++s) {
           if (!SG && s % 8 == 0) asm volatile("" ::: "memory");  // table loads in chunks of 8 (registers)
           const float2 g = SG ? grow[lane + 32 * s] : __ldg(grow + lane + 32 * s);
-          const uint32_t kb = (MODE == MODE_ROWB) ? k1 + ((uint32_t)(lane + 32 * s) << P1) : (uint32_t)(lane + 32 * s);
-          const float rf = phase_cycles(pr, g, kb, n, a.fc, a.fs_over_n);
+          const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
+          ex |= phase_needs_exact(pr.nu_hi, g) ? (1u << s) : 0u;
           const float2 w = expm2pi((VAR == VAR_DISTORT) ? -rf : rf);
           v[s] = cmul(v[s], make_float2(w.x * inv_n, w.y * inv_n));
           if constexpr (VAR == VAR_COMPRESS) v[s] = cmul(v[s], rc[s]);
         }
+        phase_exact_fixup<VAR == VAR_DISTORT>(
+            v, ex, wk, lane, pr, grow,
+            [&](int s) {
+              return (long long)((MODE == MODE_ROWB) ? k1 + ((uint32_t)(lane + 32 * s) << P1) : (uint32_t)(lane + 32 * s));
+            },
+            n, a.fc, a.fs_over_n);
       }
       if constexpr (SG) {
         __syncwarp();  // g staging consumed: prefetch the next g row

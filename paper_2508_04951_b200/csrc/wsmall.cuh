@@ -96,13 +96,18 @@ __global__ void __launch_bounds__(kWsT, 1) warp_small_kernel(const WarpArgs a) {
       wfft1024<false>(v, wk, Tw, lane);
       const PulseParams pr = a.pp[a.pulse_base + p0 + pl];
       const float2 *grow = a.gtab + 1024 * k1;
+      uint32_t ex = 0u;  // elements needing the exact binary64 phase (phase_exact_fixup)
 #pragma unroll
       for (int s = 0; s < 32; ++s) {
         if (s % 8 == 0) asm volatile("" ::: "memory");  // table loads in chunks of 8 (registers)
-        const float rf = phase_cycles(pr, __ldg(grow + lane + 32 * s), k1 + (int64_t)N1 * (lane + 32 * s), n, a.fc,
-                                      a.fs_over_n);
+        const float2 g = __ldg(grow + lane + 32 * s);
+        const float rf = phase_frac(pr.nu_hi, pr.nu_lo, g);
+        ex |= phase_needs_exact(pr.nu_hi, g) ? (1u << s) : 0u;
         v[s] = cmul(v[s], expm2pi((VAR == VAR_DISTORT) ? -rf : rf));
       }
+      phase_exact_fixup<VAR == VAR_DISTORT>(
+          v, ex, wk, lane, pr, grow, [&](int s) { return (long long)k1 + (long long)N1 * (lane + 32 * s); }, n, a.fc,
+          a.fs_over_n);
       wfft1024<true>(v, wk, Tw, lane);
       __syncwarp();
       Pw[lane] = twn((32u * (uint32_t)k1 * (uint32_t)lane) & nmask, log2n);
