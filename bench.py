@@ -125,6 +125,17 @@ def physical_gpu(local_rank: int) -> int:
     return local_rank
 
 
+def cpu_model() -> str:
+    """The host CPU model (lscpu "Model name", from /proc/cpuinfo)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_rate(bank, index, tec, alpha, n, taps, pulses_sample: int, threads: int):
     """Time the FP64 oracle (as it stands) on a bounded sample of the workload."""
     from oracle import oracle as O
@@ -164,7 +175,8 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "pulses": pulses, "n": n, "taps": taps, "fs_hz": FS},
         "rtf": value / FS,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -181,6 +193,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--warmup-ref", type=int, default=1)
+    ap.add_argument("--dump-sample", default="", help="write the gathered C4 parity-sample outputs (npz) on rank 0")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -193,9 +206,18 @@ def main():
     from paper_2508_04951_b200 import build as dcbuild
 
     ws, rank, local = dist_info()
+    # one process per GPU over NCCL; DISPCORR_BENCH_BACKEND=gloo lets a test run several ranks on one GPU
+    backend = os.environ.get("DISPCORR_BENCH_BACKEND", "nccl")
+    gpu = local % max(1, torch.cuda.device_count())
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) in the run log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
+    torch.cuda.set_device(gpu)
+    red_dev = "cuda" if backend == "nccl" else None
     if rank == 0:
         dcbuild.build()
     if ws > 1:
@@ -227,7 +249,7 @@ def main():
 
     # ---------------- timed region (device-resident inputs; 8 GiB per rank at N=1 >> 126 MB L2)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(physical_gpu(local)) as clk:
+    with ClockSampler(physical_gpu(gpu)) as clk:
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -240,7 +262,7 @@ def main():
         if ws > 1:
             dist.barrier()
         launches = plan.info()["kernel_launches"] - l0
-    ms = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
+    ms = max_over_ranks(ev0.elapsed_time(ev1), device=red_dev)
     value = pulses * n * args.steps / (ms / 1e3)
     clocks = clk.summary()
 
@@ -261,7 +283,7 @@ def main():
             gbs = 16.0 * d["samples"] / sec / 1e9  # algorithmic: read 8 B + write 8 B per sample
             out[name] = {"launches": d["launches"], "ms_per_launch": d["ms"] / d["launches"],
                          "samples_per_launch": d["samples"] // d["launches"], "gbs": gbs, "frac_hbm": gbs / hbm}
-            if name in ("doppler", "fused"):
+            if name == "doppler":
                 tfl = 4.0 * taps * d["samples"] / sec / 1e12
                 out[name]["tflops_sinc"] = tfl
                 out[name]["frac_fp32"] = tfl / (148 * 128 * 2 * sm_max * 1e6 / 1e12)
@@ -271,7 +293,7 @@ def main():
     stages = None
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches"])
     src = stages if stages else kern
-    fft_names = [k for k in src if k not in ("doppler", "fused")]
+    fft_names = [k for k in src if k not in ("doppler", "pq")]
     fft_stage = None
     if fft_names:
         fft_ms = sum(src[k]["ms_per_launch"] * src[k]["launches"] for k in fft_names)
@@ -285,7 +307,7 @@ def main():
     tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
     tfile = tfiles[-1] if tfiles else ""  # the latest round's capture of the kernels as built
     kname = {"fourstep_A": "warp_col3_kernel<0>", "fourstep_B": "warp_row_kernel<2", "fourstep_C": "warp_col3_kernel<1>",
-             "doppler": "doppler_pipe_kernel<0, 32, 0>", "fused": "fused_correct_kernel<0, 32>"}.get(dom)
+             "doppler": "doppler_pipe_kernel<0, 32, 0>"}.get(dom)
     if os.path.exists(tfile) and kname and n == (1 << 20):
         per = json.load(open(tfile))["dram_bytes_per_sample"]
         hit = [v for k, v in per.items() if kname in k]
@@ -309,22 +331,41 @@ def main():
         for _ in range(args.e2e_steps):
             plan.correct_host(xh, yh, tec_r, alpha_r)
         torch.cuda.synchronize()
-        el = max_over_ranks(time.perf_counter() - t0, device="cuda")
+        el = max_over_ranks(time.perf_counter() - t0, device=red_dev)
         e2e = {"value": pulses * n * args.e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(xh.numel() * 8 * ws), "d2h_bytes_per_step": int(yh.numel() * 8 * ws),
                "steps": args.e2e_steps, "api": "dc_correct_host (pinned host buffers, chunked H2D/compute/D2H overlap)"}
-        # the e2e output must equal the device path bit for bit
-        same = bool(torch.equal(yh, y.cpu())) if my <= 64 else None
+        # the e2e output must equal the device path bit for bit (sampled pulses of this rank's shard)
+        sel = sorted({0, my // 3, my // 2, my - 1}) if my > 0 else []
+        same = all(bool(torch.equal(yh[i], y[i].cpu())) for i in sel)
         e2e["matches_device_path"] = same
+        e2e["matches_checked_pulses"] = len(sel)
         del xh, yh
 
-    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    # ---------------- parity sample (optional): the C4 sample pulses gathered to rank 0 for a test to check
+    if args.dump_sample:
+        sample = [p for p in (list(range(0, pulses, 64)) + [1, 511, 1023]) if p < pulses]
+        mine = [p for p in sample if lo <= p < hi]
+        ys = torch.stack([y[p - lo] for p in mine]).cpu() if mine else torch.zeros((0, n), dtype=torch.complex64)
+        parts = [None] * ws
+        if ws > 1:
+            dist.all_gather_object(parts, (mine, ys.numpy()))
+        else:
+            parts = [(mine, ys.numpy())]
+        if rank == 0:
+            idx = [p for part in parts for p in part[0]]
+            arr = np.concatenate([part[1] for part in parts], axis=0)
+            np.savez(args.dump_sample, pulses=np.array(idx), y=arr, shards=np.array(
+                [shard_range(pulses, r, ws) for r in range(ws)]))
+
+    # ---------------- CPU oracle baseline (rank 0; at N > 1 the same bounded sample on rank 0's host)
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         cores = os.cpu_count() or 1
         k = max(1, min(pulses, 2 * cores))
         rate, dt = cpu_oracle_rate(bank, index, tec, alpha, n, taps, k, cores)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+               "nproc": os.cpu_count(),
                "sample": f"first {k} pulses x 2^{log2n} of the {args.config} train, dc_correct in FP64 "
                          f"(oracle.run_batch, OpenMP over pulses), {dt:.1f} s"}
 
@@ -335,7 +376,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "pulses": pulses, "n": n, "taps": taps, "fs_hz": FS,
                        "parallelism": f"pulse-sharded x{ws} (no data-path collective)",
-                       "l2": "inputs 8 GiB/rank at N=1 (>> 126 MB L2); no flush needed"},
+                       "l2": f"inputs {my * n * 8 / 2**30:.1f} GiB on rank 0 (>> 126 MB L2); no flush needed"},
             "rtf": value / FS, "rtf_per_gpu": value / FS / ws,
             "gpu_launches": int(launches),
             "clocks": clocks,

@@ -91,8 +91,7 @@ dc_status dc_iono_distort(dc_plan_t plan, void *x, int64_t batch, const double *
  * r: device float2[L], 1 <= L <= n, the transmitted reference r_0 .. r_{L-1}; it is
  * zero-padded to n and its DFT R_k is computed on the device and kept (conjugated) in
  * the plan (8n bytes), replacing any earlier reference.  r may be reused as soon as
- * the plan's stream has passed this call.  Supported for n = 2^10 and n = 2^14 .. 2^21
- * (the warp-level row-FFT regimes); other n return DC_ERR_INVALID_VALUE. */
+ * the plan's stream has passed this call.  Any plan size n. */
 dc_status dc_set_reference(dc_plan_t plan, const void *r, int64_t L);
 
 /* Pulse compression after the ionospheric correction (reading R16):
@@ -101,7 +100,7 @@ dc_status dc_set_reference(dc_plan_t plan, const void *r, int64_t L);
  * Eq. 15 phase step, so compression costs no HBM bytes beyond dc_iono's.
  * x, z: device float2[batch][n]; z == x (in place) or z disjoint from x (else
  * DC_ERR_ALIASING).  tec: host double[batch] as dc_iono.  DC_ERR_INVALID_VALUE when no
- * reference has been set or n is unsupported (see dc_set_reference). */
+ * reference has been set. */
 dc_status dc_compress(dc_plan_t plan, const void *x, void *z, int64_t batch, const double *tec);
 
 /* Doppler correction: y[p][m] = e^{-i 2 pi fc (1 - beta) m / fs} *
@@ -111,6 +110,21 @@ dc_status dc_compress(dc_plan_t plan, const void *x, void *z, int64_t batch, con
  * x, y: device float2[batch][n], must not overlap.  alpha: host double[batch], each finite > 0.
  * alpha[p] == 1 reproduces x[p] bit-exactly. */
 dc_status dc_doppler(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *alpha);
+
+/* Doppler correction by FFT P/Q resampling, the paper's second resampling method ("the Fourier
+ * transform of the signal has terms removed or added followed by an inverse Fourier transform",
+ * P:L206; box filter of N/alpha samples, exact when N - N/alpha is an even integer, P:L292-294;
+ * benchmarked in fig:pqbenchmark).  Reading R18, per pulse p:
+ *   M = n + 2 round((n alpha[p] - n) / 2)   (an even number of samples added or removed)
+ *   X = DFT_n(x[p]);  Y = X with the bins of |signed frequency| >= min(n, M)/2 removed (M < n: the
+ *   -Nyquist bin folded into +Nyquist) or zeros added (M > n: the Nyquist bin split in half over +-);
+ *   y[p][m] = (1/n) sum_k Y_k e^{+i 2 pi k m / M} * e^{-i 2 pi fc (1 - n/M) m / fs}  for m < min(n, M),
+ *   0 for min(n, M) <= m < n.  M == n (|n alpha - n| < 1) returns x[p] bit-exactly (no work).
+ * The length-M inverse DFT is a chirp-z (Bluestein) convolution of length 2n on the device.
+ * x, y: device float2[batch][n], must not overlap.  alpha: host double[batch], finite > 0, with
+ * 2 <= M <= 8n.  n <= 2^23.  The plan keeps a cache of per-M convolution tables (16n bytes each,
+ * <= 1 GiB) and 1 GiB-bounded group buffers, allocated on the first call. */
+dc_status dc_doppler_pq(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *alpha);
 
 /* Taper of the Doppler stage's sinc window (reading R17; "taper window size, taper"):
  * Kaiser window of shape `kaiser` over the W = taps window, half-width L = W/2,
@@ -152,9 +166,9 @@ dc_status dc_plan_info(dc_plan_t plan, dc_plan_info_t *info);
  * synchronises the stream and returns, per class, the launches, summed device milliseconds and
  * samples processed since the last reset.  Classes: DC_K_IONO_SMALL (regime-0 fused FFT ->
  * phase -> IFFT), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler),
- * DC_K_FUSED (the single persistent dc_correct kernel used for n = 2^20). */
+ * DC_K_PQ (one record per dc_doppler_pq launch group: all of its kernels). */
 enum { DC_K_IONO_SMALL = 0, DC_K_FOURSTEP_A = 1, DC_K_FOURSTEP_B = 2, DC_K_FOURSTEP_C = 3, DC_K_DOPPLER = 4,
-       DC_K_FUSED = 5, DC_K_CLASSES = 6 };
+       DC_K_PQ = 5, DC_K_CLASSES = 6 };
 typedef struct {
   int64_t launches[DC_K_CLASSES];
   double ms[DC_K_CLASSES];

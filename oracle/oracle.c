@@ -359,16 +359,10 @@ int orc_doppler_exact(int64_t n, double fs, double fc, double alpha, const doubl
  * i.e. the band-limited periodic interpolant of x at t = m n / M (scipy.signal.resample's
  * convention).  Direct transforms of any length (the definitions written out).
  * ------------------------------------------------------------------------- */
-int orc_pq_resample(int64_t n, int64_t M, const double *x, double *y) {
-  if (n < 1 || M < 1) return -1;
-  double *X = (double *)malloc(sizeof(double) * 2 * (size_t)n);
-  double *Y = (double *)calloc(2 * (size_t)M, sizeof(double));
-  if (!X || !Y) {
-    free(X);
-    free(Y);
-    return -2;
-  }
-  orc_dft(n, x, X, -1);
+/* The length-M spectrum Y of the P/Q resampler from the length-n spectrum X (reading R18): bins
+ * 0 .. Nm/2 and -1 .. -(Nm - Nm/2 - 1) copied (Nm = min(n, M)); for even Nm the Nyquist bin is folded
+ * (M < n: X[-h] added into Y[+h]) or split in half over Y[+h] and Y[-h] (M > n).  Y: 2M doubles, zeroed. */
+static void pq_bins(int64_t n, int64_t M, const double *X, double *Y) {
   const int64_t Nm = (n < M) ? n : M;
   const int64_t nyq = Nm / 2 + 1;               /* bins 0 .. nyq-1: DC, positive (and +Nm/2 when even) */
   for (int64_t k = 0; k < nyq; ++k) {
@@ -391,6 +385,19 @@ int orc_pq_resample(int64_t n, int64_t M, const double *x, double *y) {
       Y[2 * (M - h) + 1] = Y[2 * h + 1];
     }
   }
+}
+
+int orc_pq_resample(int64_t n, int64_t M, const double *x, double *y) {
+  if (n < 1 || M < 1) return -1;
+  double *X = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+  double *Y = (double *)calloc(2 * (size_t)M, sizeof(double));
+  if (!X || !Y) {
+    free(X);
+    free(Y);
+    return -2;
+  }
+  orc_dft(n, x, X, -1);
+  pq_bins(n, M, X, Y);
   double *z = (double *)malloc(sizeof(double) * 2 * (size_t)M);
   if (!z) {
     free(X);
@@ -405,6 +412,41 @@ int orc_pq_resample(int64_t n, int64_t M, const double *x, double *y) {
   free(X);
   free(Y);
   free(z);
+  return 0;
+}
+
+/* orc_pq_resample at the `count` output indices idx[] only (for pulses too long for the O(n^2) DFTs):
+ * X by the radix-2 FFT (n a power of two), Y as above, then each requested output as the length-M
+ * inverse DFT sum written out, y_m = (1/n) sum_k Y_k e^{+i 2 pi (k m mod M) / M} (0 for m >= M). */
+int orc_pq_resample_at(int64_t n, int64_t M, const double *x, int64_t count, const int64_t *idx, double *y) {
+  if (n < 1 || M < 1 || (n & (n - 1))) return -1;
+  double *X = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+  double *Y = (double *)calloc(2 * (size_t)M, sizeof(double));
+  if (!X || !Y) {
+    free(X);
+    free(Y);
+    return -2;
+  }
+  memcpy(X, x, sizeof(double) * 2 * (size_t)n);
+  orc_fft(n, X, -1);
+  pq_bins(n, M, X, Y);
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t m = idx[i];
+    double re = 0.0, im = 0.0;
+    if (m < M) {
+      for (int64_t k = 0; k < M; ++k) {
+        const int64_t km = (int64_t)(((__int128)k * m) % M);
+        const double ang = 2.0 * ORC_PI * (double)km / (double)M;
+        const double c = cos(ang), s = sin(ang);
+        re += Y[2 * k] * c - Y[2 * k + 1] * s;
+        im += Y[2 * k] * s + Y[2 * k + 1] * c;
+      }
+    }
+    y[2 * i] = re / (double)n;
+    y[2 * i + 1] = im / (double)n;
+  }
+  free(X);
+  free(Y);
   return 0;
 }
 
@@ -430,6 +472,28 @@ int orc_doppler_pq(int64_t n, double fs, double fc, double alpha, const double *
     double re = y[2 * m], im = y[2 * m + 1];
     y[2 * m] = re * c - im * sn;
     y[2 * m + 1] = re * sn + im * c;
+  }
+  return 0;
+}
+
+/* orc_doppler_pq at the output indices idx[] only (orc_pq_resample_at, then the same carrier term). */
+int orc_doppler_pq_at(int64_t n, double fs, double fc, double alpha, const double *x, int64_t count, const int64_t *idx,
+                      double *y) {
+  if (n < 1 || !(alpha > 0.0)) return -1;
+  const int64_t M = orc_pq_length(n, alpha);
+  if (M < 1) return -1;
+  int rc = orc_pq_resample_at(n, M, x, count, idx, y);
+  if (rc) return rc;
+  const double beta_eff = (double)n / (double)M;
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t m = idx[i];
+    double psi = fc * (1.0 - beta_eff) * (double)m / fs;
+    double r = psi - nearbyint(psi);
+    double ang = -2.0 * ORC_PI * r;
+    double c = cos(ang), sn = sin(ang);
+    double re = y[2 * i], im = y[2 * i + 1];
+    y[2 * i] = re * c - im * sn;
+    y[2 * i + 1] = re * sn + im * c;
   }
   return 0;
 }

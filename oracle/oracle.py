@@ -75,6 +75,10 @@ def _load():
         lib.orc_pq_length.argtypes = [i64, d]
         lib.orc_doppler_pq.restype = i32
         lib.orc_doppler_pq.argtypes = [i64, d, d, d, p, p]
+        lib.orc_pq_resample_at.restype = i32
+        lib.orc_pq_resample_at.argtypes = [i64, i64, p, i64, p, p]
+        lib.orc_doppler_pq_at.restype = i32
+        lib.orc_doppler_pq_at.argtypes = [i64, d, d, d, p, i64, p, p]
         lib.orc_doppler_exact.restype = i32
         lib.orc_doppler_exact.argtypes = [i64, d, d, d, p, p]
         lib.orc_run_batch.restype = i32
@@ -214,6 +218,28 @@ def doppler_pq(x, fs: float, fc: float, alpha: float) -> np.ndarray:
     rc = _load().orc_doppler_pq(x.size, fs, fc, alpha, _ptr(x), _ptr(y))
     if rc:
         raise RuntimeError(f"orc_doppler_pq failed ({rc})")
+    return y
+
+
+def pq_resample_at(x, M: int, idx) -> np.ndarray:
+    """pq_resample(x, M) at the output indices idx only (radix-2 FFT forward; n a power of two)."""
+    x = _c128(x)
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+    y = np.empty(idx.size, dtype=np.complex128)
+    rc = _load().orc_pq_resample_at(x.size, int(M), _ptr(x), idx.size, idx.ctypes.data, _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_pq_resample_at failed ({rc})")
+    return y
+
+
+def doppler_pq_at(x, fs: float, fc: float, alpha: float, idx) -> np.ndarray:
+    """doppler_pq(x, fs, fc, alpha) at the output indices idx only."""
+    x = _c128(x)
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+    y = np.empty(idx.size, dtype=np.complex128)
+    rc = _load().orc_doppler_pq_at(x.size, fs, fc, alpha, _ptr(x), idx.size, idx.ctypes.data, _ptr(y))
+    if rc:
+        raise RuntimeError(f"orc_doppler_pq_at failed ({rc})")
     return y
 
 

@@ -12,6 +12,7 @@ raised.
     plan.doppler(x, y, alpha)         # y = resampled onto t/alpha (Eq. 16, windowed)
     plan.correct(x, y, tec, alpha)    # both stages, iono first
     plan.set_reference(r); plan.compress(x, z, tec)   # iono correction + matched filter (fused)
+    plan.doppler_pq(x, y, alpha)      # FFT P/Q resampling (the paper's second Doppler method)
 """
 from __future__ import annotations
 
@@ -40,7 +41,7 @@ class DispCorrError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
-KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler", "fused")
+KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler", "pq")
 
 
 class Profile(ctypes.Structure):
@@ -84,6 +85,7 @@ def load():
         "dc_iono": ([p, p, i64, pd], i32),
         "dc_iono_distort": ([p, p, i64, pd], i32),
         "dc_doppler": ([p, p, p, i64, pd], i32),
+        "dc_doppler_pq": ([p, p, p, i64, pd], i32),
         "dc_set_reference": ([p, p, i64], i32),
         "dc_set_taper": ([p, d], i32),
         "dc_compress": ([p, p, p, i64, pd], i32),
@@ -285,6 +287,17 @@ class Plan:
         alpha_a, pa = _f64(alpha, batch, "alpha")
         self._follow_stream()
         _check(load().dc_doppler(self._h, px, py, batch, pa))
+        return y
+
+    def doppler_pq(self, x, y, alpha):
+        """FFT P/Q resampling of x (M = n + 2 round((n alpha - n)/2) samples, reading R18) into y."""
+        px, batch = _dev_ptr(x, "x", self.n)
+        py, by = _dev_ptr(y, "y", self.n)
+        if by != batch:
+            raise ValueError("x and y batch sizes differ")
+        alpha_a, pa = _f64(alpha, batch, "alpha")
+        self._follow_stream()
+        _check(load().dc_doppler_pq(self._h, px, py, batch, pa))
         return y
 
     def correct(self, x, y, tec, alpha):

@@ -37,11 +37,12 @@ struct IonoSmallArgs {
   const float2 *tw1024;  // 1024-point pass-2 table for the warp-level kernels (n = 1024), or null
   int grid_cap;          // max CTAs of the persistent grid (0: one wave of the whole GPU)
   const float2 *gtab;    // per-bin 1/f_k FP32 pairs for the warp-level kernel, or null
-  const float2 *ref;     // var 2: conj reference spectrum (natural order), else null
-  float2 *ref_out;       // var 3: conj spectrum output, else null
+  const float2 *ref;     // var 2: T = conj(R) tables (natural bin order, n entries each), else null
+  const int *ref_idx;    // var 2: per-pulse table index (pre-offset like pp), or null = table 0
+  float2 *ref_out;       // var 3: conj spectrum output per pulse (natural order), else null
 };
-// var: 0 Eq. 15 correction, 1 Eq. 14 distortion, 2 correction + matched filter (conj(R_k) table `ref`),
-// 3 forward spectrum of one pulse stored conjugated to `ref_out` (warp-level regimes only for 2, 3)
+// var: 0 Eq. 15 correction, 1 Eq. 14 distortion, 2 correction + matched filter (T table `ref`),
+// 3 forward spectra stored conjugated to `ref_out` (no inverse transform)
 cudaError_t launch_iono_small(const IonoSmallArgs &a, int var);
 
 struct FourStepArgs {
@@ -61,8 +62,9 @@ struct FourStepArgs {
   const float2 *tw1024;       // 1024-point pass-2 table for the warp-level kernels, or null
   int grid_cap;               // max CTAs of the persistent grid (0: one wave of the whole GPU)
   const float2 *gtab;         // per-bin 1/f_k FP32 pairs (row layout) for the warp-level row kernel
-  const float2 *ref;          // var 2: conj reference spectrum in the row layout of gtab, else null
-  float2 *ref_out;            // var 3: conj spectrum output (row layout), else null
+  const float2 *ref;          // var 2: T = conj(R) tables in the row layout (k1 N2 + k2), n entries each
+  const int *ref_idx;         // var 2: per-pulse table index (indexed like pp), or null = table 0
+  float2 *ref_out;            // var 3: conj spectra per pulse (row layout), else null
 };
 // offset (float2 entries) of the NS = 32 section inside the P = 10, radix-32 forward pass table
 int tw1024_offset();
@@ -99,5 +101,12 @@ constexpr int kDopMaxCtas = 1024;                       // persistent Doppler gr
 constexpr size_t kDopDescBytes = (size_t)kDopMaxCtas * 4 * 48;
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
 int doppler_path(double max_abs_beta_m1, bool taper = false);
+
+// FFT P/Q resampling (pq_kernels.cu, reading R18).  Mv: per-pulse length M (device int[pulses]).
+cudaError_t launch_pq_gather(const float2 *Xc, float2 *a, int64_t pulses, int log2n, int P1, const int *Mv,
+                             cudaStream_t st);
+cudaError_t launch_pq_chirp(float2 *r, int64_t n, int64_t M, cudaStream_t st);
+cudaError_t launch_pq_post(const float2 *c, const float2 *x, float2 *y, int64_t pulses, int log2n, const int *Mv,
+                           double fc, double fs, cudaStream_t st);
 
 }  // namespace dc

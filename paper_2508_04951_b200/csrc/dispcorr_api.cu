@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -105,6 +106,21 @@ struct dc_plan_s {
   dc::TaperCoef tc{};
   int taper_terms = dc::kTaperTerms;
   bool ref_set = false;
+  // FFT P/Q resampling (dc_doppler_pq, reading R18): the length-2n chirp-z convolution runs on an inner
+  // plan of size 2n in its pulse-compression mode with one table T_M per P/Q length M (LRU cache)
+  dc_plan_s *pq = nullptr;
+  float2 *pq_tabs = nullptr;           // pq_cap tables of 2n entries
+  int pq_cap = 0;
+  std::vector<int64_t> pq_tab_M;       // M held by each table slot (0: empty)
+  std::vector<uint64_t> pq_tab_use;    // LRU stamps
+  uint64_t pq_clock = 0;
+  float2 *pq_X = nullptr, *pq_a = nullptr;  // group buffers: forward spectra (pq_group x n), convolution (x 2n)
+  int64_t pq_group = 0;
+  PulseParams *pq_zero = nullptr;      // tec = 0 parameters of the inner plan (pq_group entries)
+  int *pq_host = nullptr, *pq_dev = nullptr;  // per-pulse [table slot x batch][M x batch] staging
+  int64_t pq_stage_cap = 0;
+  cudaEvent_t pq_done = nullptr;
+  bool pq_used = false;
   float2 *scratch = nullptr;  // launch-group buffer of dc_correct: chunk * n samples
   void *dop_desc = nullptr;   // Doppler kernel: per-CTA tile-geometry slots (dc::kDopDescBytes)
   int64_t scratch_bytes = 0;
@@ -354,13 +370,19 @@ struct DeviceGuard {
   if (dev_guard_.err != cudaSuccess) return cuda_fail(dev_guard_.err, "cudaSetDevice")
 
 // ---- stage launchers (no validation) -----------------------------------------------------------
-// var: 0 Eq. 15, 1 Eq. 14, 2 Eq. 15 + matched filter, 3 conj reference spectrum into p->ref
+// bin tables of var 2 (T tables + per-pulse index, indexed like pp) and the spectrum output of var 3
+struct RefArgs {
+  const float2 *ref = nullptr;
+  const int *ref_idx = nullptr;
+  float2 *ref_out = nullptr;
+};
+// var: 0 Eq. 15, 1 Eq. 14, 2 Eq. 15 + matched filter (tables ra.ref), 3 conj spectra into ra.ref_out
 dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
-                   int64_t pulse_base, int var, Lane ln) {
+                   int64_t pulse_base, int var, Lane ln, RefArgs ra = RefArgs{}) {
   if (p->regime == 0) {
     dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp ? pp + pulse_base : nullptr, p->tw_small_f, p->tw_small_i,
-                        p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab, p->ref,
-                        var == 3 ? p->ref : nullptr};
+                        p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab, ra.ref,
+                        ra.ref_idx ? ra.ref_idx + pulse_base : nullptr, ra.ref_out};
     ProfScope ps(p, DC_K_IONO_SMALL, pulses * p->n, ln.st);
     DC_CUDA(dc::launch_iono_small(a, var), "iono_small_kernel launch");
     return DC_OK;
@@ -386,18 +408,14 @@ dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses,
   a.tw1024 = p->tw1024;
   a.grid_cap = ln.cap;
   a.gtab = p->gtab;
-  a.ref = p->ref;
-  a.ref_out = (var == 3) ? p->ref : nullptr;
+  a.ref = ra.ref;
+  a.ref_idx = ra.ref_idx;
+  a.ref_out = ra.ref_out;
   for (int pass = 0; pass < (var == 3 ? 2 : 3); ++pass) {
     ProfScope ps(p, DC_K_FOURSTEP_A + pass, pulses * p->n, ln.st);
     DC_CUDA(dc::launch_iono_fourstep_pass(a, pass, var), "four-step kernel launch");
   }
   return DC_OK;
-}
-
-// pulse compression (var 2/3) runs on the warp-level row kernel: n = 2^10 or 2^14 .. 2^21
-bool compress_supported(const dc_plan_s *p) {
-  return p->tw1024 && p->gtab && ((p->regime == 0 && p->log2n == 10) || (p->regime == 1 && p->P2 == 10));
 }
 
 dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
@@ -436,11 +454,8 @@ dc_status iono_common(dc_plan_t p, const void *x, void *z, int64_t batch, const 
     if ((s = check_overlap(x, z, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
   }
   if ((s = check_tec(tec, batch)) != DC_OK) return s;
-  if (var == 2) {
-    if (!compress_supported(p))
-      return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^14 .. 2^21 (plan n = %lld)", (long long)p->n);
-    if (!p->ref_set) return fail(DC_ERR_INVALID_VALUE, "no matched-filter reference: call dc_set_reference first");
-  }
+  if (var == 2 && !p->ref_set)
+    return fail(DC_ERR_INVALID_VALUE, "no matched-filter reference: call dc_set_reference first");
   DC_DEVICE_GUARD(p);
   PulseParams *pp;
   ParamSlot *slot;
@@ -450,7 +465,8 @@ dc_status iono_common(dc_plan_t p, const void *x, void *z, int64_t batch, const 
   const int64_t step = (p->regime == 0) ? std::min<int64_t>(batch, 1ll << 30) : p->chunk;
   for (int64_t b0 = 0; b0 < batch && s == DC_OK; b0 += step) {
     const int64_t nb = std::min(step, batch - b0);
-    s = run_iono(p, xp + b0 * p->n, zp + b0 * p->n, nb, pp, b0, var, Lane{p->stream, 0});
+    s = run_iono(p, xp + b0 * p->n, zp + b0 * p->n, nb, pp, b0, var, Lane{p->stream, 0},
+                 RefArgs{var == 2 ? p->ref : nullptr, nullptr, nullptr});
   }
   return release_after(p, slot, s);
 }
@@ -608,6 +624,11 @@ dc_status dc_plan_destroy(dc_plan_t p) {
                     p->scratch, p->gtab, p->ref, p->hin[0], p->hin[1], p->hout[0], p->hout[1]};
   for (float2 *b : bufs)
     if (b) cudaFree(b);
+  if (p->pq) dc_plan_destroy(p->pq);
+  for (void *b : {(void *)p->pq_tabs, (void *)p->pq_X, (void *)p->pq_a, (void *)p->pq_zero, (void *)p->pq_dev})
+    if (b) cudaFree(b);
+  if (p->pq_host) cudaFreeHost(p->pq_host);
+  if (p->pq_done) cudaEventDestroy(p->pq_done);
   for (auto &s : p->ring) {
     if (s.done) cudaEventDestroy(s.done);
     if (s.host) cudaFreeHost(s.host);
@@ -658,8 +679,6 @@ dc_status dc_iono_distort(dc_plan_t p, void *x, int64_t batch, const double *tec
 dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
   dc_status s;
-  if (!compress_supported(p))
-    return fail(DC_ERR_INVALID_VALUE, "pulse compression needs n = 2^10 or 2^14 .. 2^21 (plan n = %lld)", (long long)p->n);
   if (L < 1 || L > p->n) return fail(DC_ERR_INVALID_VALUE, "reference length L = %lld must be in [1, n = %lld]", (long long)L, (long long)p->n);
   if ((s = check_device_ptr(p, r, "r")) != DC_OK) return s;
   DC_DEVICE_GUARD(p);
@@ -672,7 +691,9 @@ dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
   // zero-padded reference in the chunk buffer, then its forward DFT stored conjugated (var 3)
   DC_CUDA(cudaMemsetAsync(p->scratch, 0, (size_t)p->n * sizeof(float2), p->stream), "cudaMemsetAsync");
   DC_CUDA(cudaMemcpyAsync(p->scratch, r, (size_t)L * sizeof(float2), cudaMemcpyDeviceToDevice, p->stream), "cudaMemcpyAsync");
-  if ((s = run_iono(p, p->scratch, p->scratch, 1, nullptr, 0, 3, Lane{p->stream, 0})) != DC_OK) return s;
+  if ((s = run_iono(p, p->scratch, p->scratch, 1, nullptr, 0, 3, Lane{p->stream, 0}, RefArgs{nullptr, nullptr, p->ref})) !=
+      DC_OK)
+    return s;
   p->ref_set = true;
   return DC_OK;
 }
@@ -729,6 +750,157 @@ dc_status dc_doppler(dc_plan_t p, const void *x, void *y, int64_t batch, const d
     s = run_doppler(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb, Lane{p->stream, 0});
   }
   return release_after(p, slot, s);
+}
+
+dc_status dc_doppler_pq(dc_plan_t p, const void *x, void *y, int64_t batch, const double *alpha) {
+  if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  dc_status s;
+  if (p->log2n > 23) return fail(DC_ERR_INVALID_VALUE, "FFT P/Q resampling needs n <= 2^23 (plan n = %lld)", (long long)p->n);
+  if ((s = check_batch(batch)) != DC_OK) return s;
+  if ((s = check_device_ptr(p, x, "x")) != DC_OK) return s;
+  if ((s = check_device_ptr(p, y, "y")) != DC_OK) return s;
+  if ((s = check_overlap(x, y, batch * p->n * (int64_t)sizeof(float2))) != DC_OK) return s;
+  if ((s = check_alpha(alpha, batch)) != DC_OK) return s;
+  const int64_t n = p->n, L = 2 * n;
+  // P/Q length per pulse, the oracle's rounding (orc_pq_length): M = n + 2 round((n alpha - n) / 2)
+  std::vector<int64_t> Ms((size_t)batch);
+  for (int64_t i = 0; i < batch; ++i) {
+    const int64_t M = n + 2 * (int64_t)std::llround(0.5 * ((double)n * alpha[i] - (double)n));
+    if (M < 2 || M > 8 * n)
+      return fail(DC_ERR_INVALID_VALUE, "alpha[%lld] = %g gives a P/Q length M = %lld outside [2, 8n]", (long long)i,
+                  alpha[i], (long long)M);
+    Ms[(size_t)i] = M;
+  }
+  DC_DEVICE_GUARD(p);
+  // ---- lazily built state: inner plan of size 2n, table cache, group buffers, staging
+  if (!p->pq) {
+    dc_plan_t inner = nullptr;
+    if ((s = dc_plan(&inner, L, p->fs, 0.0, 2, p->device, p->stream)) != DC_OK) return s;
+    p->pq = inner;
+    p->pq_group = std::max<int64_t>(1, std::min<int64_t>(4096, (1ll << 30) / (n * (int64_t)sizeof(float2))));
+    p->pq_cap = (int)std::max<int64_t>(2, std::min<int64_t>(64, (1ll << 30) / (L * (int64_t)sizeof(float2))));
+    const size_t tab_bytes = (size_t)p->pq_cap * L * sizeof(float2);
+    if (cudaMalloc(&p->pq_tabs, tab_bytes) != cudaSuccess ||
+        cudaMalloc(&p->pq_X, (size_t)(p->pq_group * n) * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&p->pq_a, (size_t)(p->pq_group * L) * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&p->pq_zero, (size_t)p->pq_group * sizeof(PulseParams)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DC_ERR_OUT_OF_MEMORY, "FFT P/Q buffers");
+    }
+    DC_CUDA(cudaMemsetAsync(p->pq_tabs, 0, tab_bytes, p->stream), "cudaMemsetAsync");
+    DC_CUDA(cudaMemsetAsync(p->pq_zero, 0, (size_t)p->pq_group * sizeof(PulseParams), p->stream), "cudaMemsetAsync");
+    DC_CUDA(cudaEventCreateWithFlags(&p->pq_done, cudaEventDisableTiming), "cudaEventCreate");
+    p->pq_tab_M.assign((size_t)p->pq_cap, 0);
+    p->pq_tab_use.assign((size_t)p->pq_cap, 0);
+  }
+  p->pq->stream = p->stream;
+  if (p->pq_used) DC_CUDA(cudaEventSynchronize(p->pq_done), "cudaEventSynchronize(P/Q staging)");
+  if (p->pq_stage_cap < batch) {
+    if (p->pq_host) cudaFreeHost(p->pq_host);
+    if (p->pq_dev) cudaFree(p->pq_dev);
+    p->pq_host = nullptr;
+    p->pq_dev = nullptr;
+    p->pq_stage_cap = 0;
+    const int64_t cap = std::max<int64_t>(batch, 1024);
+    if (cudaMallocHost(&p->pq_host, 2 * sizeof(int) * cap) != cudaSuccess ||
+        cudaMalloc(&p->pq_dev, 2 * sizeof(int) * cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DC_ERR_OUT_OF_MEMORY, "P/Q staging (%lld pulses)", (long long)cap);
+    }
+    p->pq_stage_cap = cap;
+  }
+  // ---- groups of consecutive pulses with at most pq_cap distinct non-identity M; tables assigned LRU
+  struct Group {
+    int64_t b0, nb;
+    std::vector<std::pair<int, int64_t>> builds;  // (slot, M) tables to build before the group
+  };
+  std::vector<Group> groups;
+  int *slot_h = p->pq_host, *M_h = p->pq_host + batch;
+  for (int64_t b0 = 0; b0 < batch;) {
+    Group g{b0, 0, {}};
+    std::vector<int64_t> need;
+    int64_t b = b0;
+    for (; b < batch && b - b0 < p->pq_group; ++b) {
+      const int64_t M = Ms[(size_t)b];
+      if (M != n && std::find(need.begin(), need.end(), M) == need.end()) {
+        if ((int)need.size() == p->pq_cap) break;
+        need.push_back(M);
+      }
+    }
+    g.nb = b - b0;
+    const uint64_t stamp = ++p->pq_clock;
+    for (int64_t M : need) {  // hits first, so that misses never evict a table this group uses
+      for (int t = 0; t < p->pq_cap; ++t)
+        if (p->pq_tab_M[(size_t)t] == M) p->pq_tab_use[(size_t)t] = stamp;
+    }
+    for (int64_t M : need) {
+      int slot = -1;
+      for (int t = 0; t < p->pq_cap && slot < 0; ++t)
+        if (p->pq_tab_M[(size_t)t] == M) slot = t;
+      if (slot < 0) {
+        uint64_t best = UINT64_MAX;
+        for (int t = 0; t < p->pq_cap; ++t)
+          if (p->pq_tab_use[(size_t)t] != stamp && p->pq_tab_use[(size_t)t] < best) {
+            best = p->pq_tab_use[(size_t)t];
+            slot = t;
+          }
+        p->pq_tab_M[(size_t)slot] = M;
+        p->pq_tab_use[(size_t)slot] = stamp;
+        g.builds.push_back({slot, M});
+      }
+    }
+    for (int64_t i = b0; i < b0 + g.nb; ++i) {
+      int slot = 0;  // identity pulses (M == n): their convolution input is zero, any table will do
+      for (int t = 0; t < p->pq_cap; ++t)
+        if (Ms[(size_t)i] != n && p->pq_tab_M[(size_t)t] == Ms[(size_t)i]) slot = t;
+      slot_h[i] = slot;
+      M_h[i] = (int)Ms[(size_t)i];
+    }
+    groups.push_back(std::move(g));
+    b0 += groups.back().nb;
+  }
+  DC_CUDA(cudaMemcpyAsync(p->pq_dev, p->pq_host, 2 * sizeof(int) * batch, cudaMemcpyHostToDevice, p->stream),
+          "cudaMemcpyAsync(P/Q staging)");
+  const int *slot_d = p->pq_dev, *M_d = p->pq_dev + batch;
+  const float2 *xp = (const float2 *)x;
+  float2 *yp = (float2 *)y;
+  const Lane ln{p->stream, 0};
+  const int P1row = (p->regime == 1) ? p->P1 : 0;  // row layout of the n-plan's spectra (natural in regime 0)
+  auto pipeline = [&]() -> dc_status {
+    dc_status st = DC_OK;
+    for (const Group &g : groups) {
+      const int64_t l0 = p->pq->launches;
+      ProfScope ps(p, DC_K_PQ, g.nb * n, ln.st);
+      for (const auto &bm : g.builds) {  // T_M = conj(DFT_L(r)), r = conj(b reflected): FFT(a) T_M = FFT(a) FFT(b)
+        DC_CUDA(dc::launch_pq_chirp(p->pq_a, n, bm.second, ln.st), "pq_chirp_kernel launch");
+        p->launches += 1;
+        if ((st = run_iono(p->pq, p->pq_a, p->pq_a, 1, nullptr, 0, 3, ln,
+                           RefArgs{nullptr, nullptr, p->pq_tabs + (size_t)bm.first * L})) != DC_OK)
+          return st;
+      }
+      // X = DFT_n(x) (stored conjugated, row layout), a = chirp-weighted kept bins, c = a (*) b, y
+      const bool prof = p->prof;  // the forward passes are part of this DC_K_PQ record, not of the four-step classes
+      p->prof = false;
+      st = run_iono(p, xp + g.b0 * n, p->pq_X, g.nb, nullptr, 0, 3, ln, RefArgs{nullptr, nullptr, p->pq_X});
+      p->prof = prof;
+      if (st != DC_OK) return st;
+      DC_CUDA(dc::launch_pq_gather(p->pq_X, p->pq_a, g.nb, p->log2n, P1row, M_d + g.b0, ln.st), "pq_gather_kernel launch");
+      if ((st = run_iono(p->pq, p->pq_a, p->pq_a, g.nb, p->pq_zero, 0, 2, ln, RefArgs{p->pq_tabs, slot_d + g.b0, nullptr})) !=
+          DC_OK)
+        return st;
+      DC_CUDA(dc::launch_pq_post(p->pq_a, xp + g.b0 * n, yp + g.b0 * n, g.nb, p->log2n, M_d + g.b0, p->fc, p->fs, ln.st),
+              "pq_post_kernel launch");
+      p->launches += 1 + (p->pq->launches - l0);  // gather + post (+1 counted by ps) + the inner plan's kernels
+    }
+    return st;
+  };
+  s = pipeline();
+  cudaEventRecord(p->pq_done, p->stream);
+  p->pq_used = true;
+  if (s != DC_OK) {  // a failed launch leaves the cache state unknown: drop it
+    std::fill(p->pq_tab_M.begin(), p->pq_tab_M.end(), 0);
+  }
+  return s;
 }
 
 dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const double *tec, const double *alpha) {
@@ -817,7 +989,7 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
       DC_CUDA(cudaEventRecord(p->ev_in[i], p->s_h2d), "record");
       DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[i], 0), "wait");
       if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[i], 0), "wait");  // hout[i] drained
-      if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, false, Lane{p->stream, 0})) != DC_OK) return s;
+      if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, 0, Lane{p->stream, 0})) != DC_OK) return s;
       if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
       DC_CUDA(cudaEventRecord(p->ev_comp[i], p->stream), "record");
       DC_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[i], 0), "wait");

@@ -35,10 +35,10 @@ static constexpr int small_nb(int P) { return (8192 >> P) < 1 ? 1 : (8192 >> P);
 static constexpr int col_c(int P1) { return (8192 >> P1) < 4 ? 4 : (8192 >> P1); }
 static constexpr int row_nb(int P2) { return (8192 >> P2) < 1 ? 1 : (8192 >> P2); }
 
-template <int P, int LOGE, int NB, bool ROW, int MODE, bool DISTORT>
+template <int P, int LOGE, int NB, bool ROW, int MODE, int VAR>
 static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_t st, int cap) {
   using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
-  auto kern = tile_fft_kernel<P, LOGE, NB, ROW, MODE, DISTORT>;
+  auto kern = tile_fft_kernel<P, LOGE, NB, ROW, MODE, VAR>;
   const size_t smem = CFG::smem_bytes(a.H, a.log2n);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -129,8 +129,7 @@ static cudaError_t launch_tcol(const WarpArgs &a, int P1, bool inv, cudaStream_t
   }
 }
 
-static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr,
-                          const float2 *ref = nullptr, float2 *ref_out = nullptr) {
+static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 *gtab = nullptr) {
   WarpArgs w{};
   w.src = t.src;
   w.dst = t.dst;
@@ -147,19 +146,29 @@ static WarpArgs warp_args(const TileArgs &t, const float2 *tw1024, const float2 
   w.fc = t.fc;
   w.scale = 1.0f / (float)(1 << t.log2n);
   w.gtab = gtab;
-  w.ref = ref;
-  w.ref_out = ref_out;
+  w.ref = t.ref;
+  w.ref_idx = t.ref_idx;
+  w.ref_out = t.ref_out;
   return w;
 }
 // pass-2 section (NS = 32, R = 32) of the P = 10, E = 32 forward table: float4 [r/2][k] layout
 static constexpr int kTw1024Off = PassPlan<10, 5>::tw_off_fwd(1);
 
-template <int P>
-static cudaError_t launch_small_p(const TileArgs &a, bool distort, cudaStream_t st, int cap) {
+template <int P, int VAR>
+static cudaError_t launch_small_pv(const TileArgs &a, cudaStream_t st, int cap) {
   constexpr int NB = small_nb(P);
   const int64_t total = (a.pulses + NB - 1) / NB;
-  return distort ? launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, true>(a, total, st, cap)
-                 : launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, false>(a, total, st, cap);
+  return launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, VAR>(a, total, st, cap);
+}
+template <int P>
+static cudaError_t launch_small_p(const TileArgs &a, int var, cudaStream_t st, int cap) {
+  switch (var) {
+    case VAR_CORRECT: return launch_small_pv<P, VAR_CORRECT>(a, st, cap);
+    case VAR_DISTORT: return launch_small_pv<P, VAR_DISTORT>(a, st, cap);
+    case VAR_COMPRESS: return launch_small_pv<P, VAR_COMPRESS>(a, st, cap);
+    case VAR_REFERENCE: return launch_small_pv<P, VAR_REFERENCE>(a, st, cap);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <int N1>
@@ -191,30 +200,32 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   a.H = 0;
   a.fs_over_n = s.fs_over_n;
   a.fc = s.fc;
+  a.ref = s.ref;
+  a.ref_idx = s.ref_idx;
+  a.ref_out = s.ref_out;
   if (s.log2n == 10 && s.tw1024 && s.gtab)
-    return launch_warp_row(warp_args(a, s.tw1024, s.gtab, s.ref, s.ref_out), true, var, s.stream, s.grid_cap);
-  if (var != VAR_CORRECT && var != VAR_DISTORT) return cudaErrorInvalidValue;  // compress: warp-level regimes only
+    return launch_warp_row(warp_args(a, s.tw1024, s.gtab), true, var, s.stream, s.grid_cap);
   // in-CTA four-step on the warp FFT (wsmall.cuh) for 4096 / 8192: +5 % / +18 % over the tile
-  // kernel; for 2048 the tile kernel is faster (128 vs 148 GS/s measured) and stays
-  if (s.log2n >= 12 && s.log2n <= 13 && s.tw1024 && s.gtab) {
+  // kernel; for 2048 the tile kernel is faster (128 vs 148 GS/s measured) and stays.  Pulse
+  // compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).
+  if (s.log2n >= 12 && s.log2n <= 13 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
     const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
     return (s.log2n == 12) ? launch_wsmall<4>(w, var, s.stream, s.grid_cap) : launch_wsmall<8>(w, var, s.stream, s.grid_cap);
   }
-  const bool distort = (var == VAR_DISTORT);
   switch (s.log2n) {
-    case 1: return launch_small_p<1>(a, distort, s.stream, s.grid_cap);
-    case 2: return launch_small_p<2>(a, distort, s.stream, s.grid_cap);
-    case 3: return launch_small_p<3>(a, distort, s.stream, s.grid_cap);
-    case 4: return launch_small_p<4>(a, distort, s.stream, s.grid_cap);
-    case 5: return launch_small_p<5>(a, distort, s.stream, s.grid_cap);
-    case 6: return launch_small_p<6>(a, distort, s.stream, s.grid_cap);
-    case 7: return launch_small_p<7>(a, distort, s.stream, s.grid_cap);
-    case 8: return launch_small_p<8>(a, distort, s.stream, s.grid_cap);
-    case 9: return launch_small_p<9>(a, distort, s.stream, s.grid_cap);
-    case 10: return launch_small_p<10>(a, distort, s.stream, s.grid_cap);
-    case 11: return launch_small_p<11>(a, distort, s.stream, s.grid_cap);
-    case 12: return launch_small_p<12>(a, distort, s.stream, s.grid_cap);
-    case 13: return launch_small_p<13>(a, distort, s.stream, s.grid_cap);
+    case 1: return launch_small_p<1>(a, var, s.stream, s.grid_cap);
+    case 2: return launch_small_p<2>(a, var, s.stream, s.grid_cap);
+    case 3: return launch_small_p<3>(a, var, s.stream, s.grid_cap);
+    case 4: return launch_small_p<4>(a, var, s.stream, s.grid_cap);
+    case 5: return launch_small_p<5>(a, var, s.stream, s.grid_cap);
+    case 6: return launch_small_p<6>(a, var, s.stream, s.grid_cap);
+    case 7: return launch_small_p<7>(a, var, s.stream, s.grid_cap);
+    case 8: return launch_small_p<8>(a, var, s.stream, s.grid_cap);
+    case 9: return launch_small_p<9>(a, var, s.stream, s.grid_cap);
+    case 10: return launch_small_p<10>(a, var, s.stream, s.grid_cap);
+    case 11: return launch_small_p<11>(a, var, s.stream, s.grid_cap);
+    case 12: return launch_small_p<12>(a, var, s.stream, s.grid_cap);
+    case 13: return launch_small_p<13>(a, var, s.stream, s.grid_cap);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -295,14 +306,24 @@ template <int P1, int MODE>
 static cudaError_t launch_col_p(const TileArgs &a, cudaStream_t st, int cap) {
   constexpr int C = col_c(P1);
   const int64_t total = a.pulses * ((1ll << (a.log2n - P1)) / C);
-  return launch_tile_cfg<P1, DC_FS_LOGE, C, false, MODE, false>(a, total, st, cap);
+  return launch_tile_cfg<P1, DC_FS_LOGE, C, false, MODE, VAR_CORRECT>(a, total, st, cap);
 }
 
-template <int P2, bool DISTORT>
-static cudaError_t launch_row_p(const TileArgs &a, cudaStream_t st, int cap) {
+template <int P2, int VAR>
+static cudaError_t launch_row_pv(const TileArgs &a, cudaStream_t st, int cap) {
   constexpr int NB = row_nb(P2);
   const int64_t total = a.pulses * ((1ll << (a.log2n - P2)) / NB);
-  return launch_tile_cfg<P2, DC_FS_LOGE, NB, true, MODE_ROWB, DISTORT>(a, total, st, cap);
+  return launch_tile_cfg<P2, DC_FS_LOGE, NB, true, MODE_ROWB, VAR>(a, total, st, cap);
+}
+template <int P2>
+static cudaError_t launch_row_p(const TileArgs &a, int var, cudaStream_t st, int cap) {
+  switch (var) {
+    case VAR_CORRECT: return launch_row_pv<P2, VAR_CORRECT>(a, st, cap);
+    case VAR_DISTORT: return launch_row_pv<P2, VAR_DISTORT>(a, st, cap);
+    case VAR_COMPRESS: return launch_row_pv<P2, VAR_COMPRESS>(a, st, cap);
+    case VAR_REFERENCE: return launch_row_pv<P2, VAR_REFERENCE>(a, st, cap);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <int MODE>
@@ -317,16 +338,15 @@ static cudaError_t launch_col(int P1, const TileArgs &a, cudaStream_t st, int ca
   }
 }
 
-template <bool DISTORT>
-static cudaError_t launch_row(int P2, const TileArgs &a, cudaStream_t st, int cap) {
+static cudaError_t launch_row(int P2, const TileArgs &a, int var, cudaStream_t st, int cap) {
   switch (P2) {
-    case 7: return launch_row_p<7, DISTORT>(a, st, cap);
-    case 8: return launch_row_p<8, DISTORT>(a, st, cap);
-    case 9: return launch_row_p<9, DISTORT>(a, st, cap);
-    case 10: return launch_row_p<10, DISTORT>(a, st, cap);
-    case 11: return launch_row_p<11, DISTORT>(a, st, cap);
-    case 12: return launch_row_p<12, DISTORT>(a, st, cap);
-    case 13: return launch_row_p<13, DISTORT>(a, st, cap);
+    case 7: return launch_row_p<7>(a, var, st, cap);
+    case 8: return launch_row_p<8>(a, var, st, cap);
+    case 9: return launch_row_p<9>(a, var, st, cap);
+    case 10: return launch_row_p<10>(a, var, st, cap);
+    case 11: return launch_row_p<11>(a, var, st, cap);
+    case 12: return launch_row_p<12>(a, var, st, cap);
+    case 13: return launch_row_p<13>(a, var, st, cap);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -334,10 +354,6 @@ static cudaError_t launch_row(int P2, const TileArgs &a, cudaStream_t st, int ca
 cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) {
   int P1, P2;
   fourstep_split(f.log2n, P1, P2);
-  // compress / reference need the warp-level row pass (N2 = 1024, n = 2^14 .. 2^21)
-  const bool warp_row = P2 == 10 && f.tw1024 && f.gtab;
-  if (var != VAR_CORRECT && var != VAR_DISTORT && !warp_row) return cudaErrorInvalidValue;
-  const bool distort = (var == VAR_DISTORT);
   TileArgs a{};
   a.pulses = f.pulses;
   a.pulse_stride = f.pulse_stride;
@@ -349,6 +365,9 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) 
   a.H = f.H;
   a.fs_over_n = f.fs_over_n;
   a.fc = f.fc;
+  a.ref = f.ref;
+  a.ref_idx = f.ref_idx;
+  a.ref_out = f.ref_out;
   switch (pass) {
     case 0:
       a.src = f.src;
@@ -363,8 +382,8 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) 
       a.twf = f.tw2f;
       a.twi = f.tw2i;
       if (P2 == 10 && f.tw1024 && f.gtab)
-        return launch_warp_row(warp_args(a, f.tw1024, f.gtab, f.ref, f.ref_out), false, var, f.stream, f.grid_cap);
-      return distort ? launch_row<true>(P2, a, f.stream, f.grid_cap) : launch_row<false>(P2, a, f.stream, f.grid_cap);
+        return launch_warp_row(warp_args(a, f.tw1024, f.gtab), false, var, f.stream, f.grid_cap);
+      return launch_row(P2, a, var, f.stream, f.grid_cap);
     case 2:
       a.src = f.dst;
       a.dst = f.dst;

@@ -31,6 +31,17 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 
 enum TileMode { MODE_SMALL = 0, MODE_COLA = 1, MODE_ROWB = 2, MODE_COLC = 3 };
 
+// What the frequency-domain step does between the forward and inverse DFTs (bins X_k):
+//   VAR_CORRECT   X_k e^{-i 2 pi nu_k}                 Eq. 15
+//   VAR_DISTORT   X_k e^{+i 2 pi nu_k}                 Eq. 14 forward model
+//   VAR_COMPRESS  X_k e^{-i 2 pi nu_k} T_k             Eq. 15 then the matched filter (reading R16);
+//                                                      T = conj(R) of the reference (per pulse: table ref_idx[p])
+//   VAR_REFERENCE store conj(X_k) to ref_out, no inverse (builds the T tables of VAR_COMPRESS; the FFT P/Q
+//                 path's forward transform)
+// Bin tables (T, ref_out) use the "row layout": bin k = k1 + N1 k2 at index k1 N2 + k2 (N1 = n / N2; natural
+// order k for single-CTA pulses, N1 = 1).
+enum RowVar { VAR_CORRECT = 0, VAR_DISTORT = 1, VAR_COMPRESS = 2, VAR_REFERENCE = 3 };
+
 struct TileArgs {
   const float2 *src;  // tile input (pulse-major, pulse_stride apart)
   float2 *dst;        // tile output
@@ -43,6 +54,9 @@ struct TileArgs {
   const float2 *twh, *twl;  // four-step outer twiddles (global; copied to smem)
   int H;
   double fs_over_n, fc;
+  const float2 *ref;    // VAR_COMPRESS: T tables (row layout), n entries each
+  const int *ref_idx;   // VAR_COMPRESS: per-pulse table index (indexed like pp), or null = table 0
+  float2 *ref_out;      // VAR_REFERENCE: conj(X) per pulse (row layout), n entries each
 };
 
 // Shared-memory layout (float2 units): [staging ELEMS][work SMEM_ELEMS][twf][twi][twh][twl]
@@ -69,7 +83,7 @@ struct TileCfg {
   }
 };
 
-template <int P, int LOGE, int NB, bool ROW, int MODE, bool DISTORT>
+template <int P, int LOGE, int NB, bool ROW, int MODE, int VAR>
 __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_fft_kernel(const TileArgs a) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
@@ -80,7 +94,8 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
   constexpr int T = CFG::T;
   constexpr int NP = PP::npass;
   constexpr bool FWD = (MODE != MODE_COLC);
-  constexpr bool INVP = (MODE != MODE_COLA);
+  constexpr bool INVP = (MODE != MODE_COLA) && VAR != VAR_REFERENCE;
+  constexpr bool DISTORT = (VAR == VAR_DISTORT);
   constexpr int R0 = 1 << (FWD ? PP::log_radix_fwd(0) : PP::log_radix_inv(0));
   extern __shared__ float4 smem4[];
   float2 *S = reinterpret_cast<float2 *>(smem4);
@@ -201,7 +216,23 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
           p = pulse;
           k1 = (int)base + b;
         }
+        if constexpr (VAR == VAR_REFERENCE) {
+          // conj(X_k) in the row layout (index k1 L + k2); ROWB undoes pass A's 1/n (exact: a power of two)
+          const float sc = (MODE == MODE_ROWB) ? (float)n : 1.0f;
+          if (p < a.pulses) {
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+              const int k2 = j + r * (L / RL);
+              const float2 x = v[q * RL + r];
+              a.ref_out[p * (int64_t)n + (int64_t)k1 * L + k2] = make_float2(x.x * sc, -x.y * sc);
+            }
+          }
+          continue;
+        }
         const double nu_coef = (p < a.pulses) ? a.pp[a.pulse_base + p].nu_coef : 0.0;
+        const float2 *tab = nullptr;
+        if constexpr (VAR == VAR_COMPRESS)
+          tab = a.ref + ((a.ref_idx && p < a.pulses) ? (int64_t)a.ref_idx[a.pulse_base + p] * n : 0) + (int64_t)k1 * L;
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
           const int k2 = j + r * (L / RL);
@@ -217,9 +248,11 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
             const float2 w = expm2pi(DISTORT ? -rf : rf);
             m = make_float2(w.x * inv_n, w.y * inv_n);
           }
+          if constexpr (VAR == VAR_COMPRESS) m = cmul(m, (p < a.pulses) ? tab[k2] : make_float2(0.f, 0.f));
           v[q * RL + r] = cmul(v[q * RL + r], m);
         }
       }
+      if constexpr (VAR == VAR_REFERENCE) continue;
     }
 
     if constexpr (INVP) run_passes<TL, PP, 0, NP - 1, true>(v, Wk, tid, CFG::SMEM_TW ? Ti : a.twi);

@@ -93,16 +93,12 @@ struct WarpArgs {
   double fs_over_n, fc;
   float scale;  // pass A: 1/n (inverse-transform normalisation folded into the outer twiddle)
   const float2 *gtab;  // per-bin 1/f_k FP32 pairs, row layout [k1][k2] (MODE_SMALL: natural order)
-  const float2 *ref;   // VAR_COMPRESS: conj(R_k) of the matched-filter reference, same layout as gtab
-  float2 *ref_out;     // VAR_REFERENCE: where conj(X_k) of the (single) input pulse is written
+  const float2 *ref;   // VAR_COMPRESS: T = conj(R_k) tables (n entries each, same layout as gtab)
+  const int *ref_idx;  // VAR_COMPRESS: per-pulse table index (indexed like pp), or null = table 0
+  float2 *ref_out;     // VAR_REFERENCE: conj(X_k) per pulse (n entries each, same layout as gtab)
 };
 
-// What the row kernel does between its forward and inverse DFTs (bins X_k of one row):
-//   VAR_CORRECT   X_k e^{-i 2 pi nu_k}                 Eq. 15
-//   VAR_DISTORT   X_k e^{+i 2 pi nu_k}                 Eq. 14 forward model
-//   VAR_COMPRESS  X_k e^{-i 2 pi nu_k} conj(R_k)       Eq. 15 then the matched filter (reading R16)
-//   VAR_REFERENCE store conj(X_k) to ref_out, no inverse (builds the conj(R_k) table of VAR_COMPRESS)
-enum RowVar { VAR_CORRECT = 0, VAR_DISTORT = 1, VAR_COMPRESS = 2, VAR_REFERENCE = 3 };
+// (RowVar: what the row kernel does between its forward and inverse DFTs -- tile_fft.cuh)
 
 // MODE_ROWB: four-step pass B on rows k1 of Z (N2 = 1024).  MODE_SMALL: whole pulses of 1024.
 // NW warps per CTA.  STAGE: each warp prefetches its next row into a private shared buffer with
@@ -209,15 +205,17 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
         // reference spectrum: X_k of the zero-padded reference pulse, stored conjugated; ROWB undoes
         // the 1/n that pass A folded in (exact: a power of two)
         const float sc = (MODE == MODE_ROWB) ? (float)n : 1.0f;
+        float2 *ro = a.ref_out + p * (int64_t)n + (int64_t)k1 * 1024;
 #pragma unroll
-        for (int s = 0; s < 32; ++s) a.ref_out[(int64_t)k1 * 1024 + lane + 32 * s] = make_float2(v[s].x * sc, -v[s].y * sc);
+        for (int s = 0; s < 32; ++s) ro[lane + 32 * s] = make_float2(v[s].x * sc, -v[s].y * sc);
       } else {
         const PulseParams pr = a.pp[a.pulse_base + p];
         const float2 *grow = SG ? (stg + 1024) : (a.gtab + (int64_t)k1 * 1024);
         float2 rc[VAR == VAR_COMPRESS ? 32 : 1];
         if constexpr (VAR == VAR_COMPRESS) {
+          const float2 *rtab = a.ref + (a.ref_idx ? (int64_t)a.ref_idx[a.pulse_base + p] * n : 0) + (int64_t)k1 * 1024;
 #pragma unroll
-          for (int s = 0; s < 32; ++s) rc[s] = __ldg(a.ref + (int64_t)k1 * 1024 + lane + 32 * s);
+          for (int s = 0; s < 32; ++s) rc[s] = __ldg(rtab + lane + 32 * s);
         }
 #pragma unroll
         uint32_t ex = 0u;  // elements needing the exact binary64 phase (phase_exact_fixup)

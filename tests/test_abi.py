@@ -27,7 +27,8 @@ def lib():
 def test_header_declares_the_hot_path_calls():
     names = declared_functions()
     for required in ("dc_plan", "dc_iono", "dc_doppler", "dc_correct", "dc_plan_destroy", "dc_status_string",
-                     "dc_alpha_from_velocity", "dc_k2_per_tec", "dc_correct_host"):
+                     "dc_alpha_from_velocity", "dc_k2_per_tec", "dc_correct_host", "dc_doppler_pq", "dc_compress",
+                     "dc_set_reference", "dc_set_taper", "dc_iono_distort"):
         assert required in names
 
 
@@ -42,6 +43,18 @@ def test_exports_are_only_the_abi(lib):
                          capture_output=True, text=True).stdout
     exported = sorted(set(l.split()[-1] for l in out.splitlines() if " T " in l))
     assert set(exported) == set(declared_functions())
+
+
+def test_library_reads_no_environment(lib):
+    # no tuning knob reaches the product path: none of libdispcorr's own objects imports getenv (the
+    # statically linked CUDA runtime reads CUDA_* variables itself; that is not library behaviour)
+    import glob
+    import subprocess
+    objs = glob.glob(os.path.join(ROOT, "paper_2508_04951_b200", "lib", "obj", "*.o"))
+    assert objs
+    for o in objs:
+        out = subprocess.run(["nm", "--undefined-only", o], capture_output=True, text=True).stdout
+        assert "getenv" not in out, o
 
 
 def test_status_strings(lib):

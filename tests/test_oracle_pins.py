@@ -586,3 +586,29 @@ def test_doppler_at_equals_whole_pulse_outputs():
         assert np.array_equal(O.doppler_at(x, 32, 51.2e6, 422e6, a, idx, kaiser=kb), y[idx])
     with pytest.raises(RuntimeError):
         O.doppler_at(x, 32, 51.2e6, 0.0, 1.0, [2048])
+
+
+# ----------------------------------------------------------------------------- P/Q at sampled outputs (R18)
+@pytest.mark.parametrize("n,M", [(64, 70), (64, 58), (256, 250), (256, 264), (1024, 1024), (512, 2)])
+def test_pq_resample_at_matches_full(n, M):
+    # the sampled-output form (radix-2 forward FFT + the length-M inverse DFT sum per output) equals the
+    # full O(n^2) definition, which is pinned to scipy.signal.resample above
+    rng = np.random.default_rng(n + 3 * M)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    idx = np.arange(n)
+    full = O.pq_resample(x, M)
+    at = O.pq_resample_at(x, M, idx)
+    assert np.abs(at - full).max() < 1e-12 * np.abs(full).max()
+
+
+@pytest.mark.parametrize("n,M", [(128, 122), (128, 134)])
+def test_doppler_pq_at_matches_full_with_carrier(n, M):
+    fs, fc = 51.2e6, 422e6
+    rng = np.random.default_rng(M)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    alpha = M / n * (1.0 + 0.3 / n)
+    assert O.pq_length(n, alpha) == M
+    idx = np.array([0, 1, 5, 63, 64, 100, n - 1])
+    full = O.doppler_pq(x, fs, fc, alpha)[idx]
+    at = O.doppler_pq_at(x, fs, fc, alpha, idx)
+    assert np.abs(at - full).max() < 1e-12 * np.abs(full).max()

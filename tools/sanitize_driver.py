@@ -62,6 +62,13 @@ if want("compress"):
         p.compress(x, z, [1e17, 2e17])
         p.compress(x, x, [1e17, 2e17])
         p.sync()
+if want("pq"):
+    for n in (256, 1 << 14, 1 << 20):                              # tile / four-step regimes of n and 2n
+        p = dc.Plan(n, FS, 422e6 if n == 256 else 0.0, taps=8)
+        x = dev(synth.complex_gaussian(n, seed=12, batch=3))
+        y = torch.empty_like(x)
+        p.doppler_pq(x, y, [(n + 2.3) / n, 1.0, (n - 4.2) / n])     # M = n + 2, identity, M = n - 4
+        p.sync()
 if want("host"):
     n = 1 << 14
     p = dc.Plan(n, FS, 0.0, taps=32)
