@@ -193,6 +193,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--warmup-ref", type=int, default=1)
+    ap.add_argument("--pulses", type=int, default=0, help="override the config's pulse count (tests)")
     ap.add_argument("--dump-sample", default="", help="write the gathered C4 parity-sample outputs (npz) on rank 0")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -225,6 +226,8 @@ def main():
     dc.load()
 
     pulses, log2n, taps, desc = CONFIGS[args.config]
+    if args.pulses:
+        pulses = args.pulses
     n = 1 << log2n
     from paper_2508_04951_b200.dist import max_over_ranks, shard_range
     lo, hi = shard_range(pulses, rank, ws)

@@ -134,6 +134,17 @@ dc_status dc_doppler_pq(dc_plan_t plan, const void *x, void *y, int64_t batch, c
  * The centre tap keeps weight 1, so alpha = 1 still reproduces x exactly. */
 dc_status dc_set_taper(dc_plan_t plan, double kaiser);
 
+/* Window of the Doppler stage's sinc taps (reading R17; "taper"), used by dc_doppler and
+ * dc_correct from the next call on, over the W = taps window with half-width L = W/2, d = t_m - k:
+ *   DC_WINDOW_RECT    h(d) = sinc(d)                                   (R11, the default; param ignored)
+ *   DC_WINDOW_KAISER  h(d) = sinc(d) I0(param sqrt(1 - (d/L)^2)) / I0(param), param in [0, 12]
+ *                     (dc_set_taper(plan, param))
+ *   DC_WINDOW_HANN    h(d) = sinc(d) (1 + cos(pi d / L)) / 2           (param ignored)
+ * The centre tap keeps weight 1, so alpha = 1 still reproduces x exactly.  DC_ERR_INVALID_VALUE for an
+ * unknown kind or a Kaiser param outside [0, 12]. */
+enum { DC_WINDOW_RECT = 0, DC_WINDOW_KAISER = 1, DC_WINDOW_HANN = 2 };
+dc_status dc_set_window(dc_plan_t plan, int kind, double param);
+
 /* dc_correct = dc_doppler(dc_iono(x)) (iono first, reading R7), x left unchanged,
  * result in y (must not overlap x).  Pulses run in launch groups of <= 2 GiB; the
  * ionospheric result of a group is kept in a plan-owned device buffer (allocated on the

@@ -268,6 +268,12 @@ double orc_kaiser(double d, double L, double kb) {
   return orc_bessel_i0(kb * sqrt(r)) / orc_bessel_i0(kb);
 }
 
+/* Hann taper (reading R17, the second taper option): taper(d) = (1 + cos(pi d / L)) / 2, selected by
+ * passing kb = ORC_HANN (-1) wherever a Kaiser kb is taken. */
+#define ORC_HANN (-1.0)
+double orc_hann(double d, double L) { return 0.5 * (1.0 + cos(ORC_PI * d / L)); }
+static double orc_taper(double d, double L, double kb) { return (kb == ORC_HANN) ? orc_hann(d, L) : orc_kaiser(d, L, kb); }
+
 /* one output m of the windowed, optionally tapered Eq. 16 with the R10 carrier (the steps above) */
 static void orc_doppler_one(int64_t n, int W, double fs, double fc, double beta, double kb, const double *x,
                             int64_t m, double *ym) {
@@ -277,7 +283,7 @@ static void orc_doppler_one(int64_t n, int W, double fs, double fc, double beta,
   double re = 0.0, im = 0.0;
   for (int64_t k = k_lo; k < k_lo + W; ++k) {
     if (k < 0 || k >= n) continue;
-    double h = orc_sinc(t - (double)k) * orc_kaiser(t - (double)k, L, kb);
+    double h = orc_sinc(t - (double)k) * orc_taper(t - (double)k, L, kb);
     re += x[2 * k] * h;
     im += x[2 * k + 1] * h;
   }
@@ -292,7 +298,7 @@ static void orc_doppler_one(int64_t n, int W, double fs, double fc, double beta,
 
 int orc_doppler_win(int64_t n, int W, double fs, double fc, double alpha, double kb,
                     const double *x, double *y) {
-  if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0)) return -1;
+  if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0 || kb == ORC_HANN)) return -1;
   double beta = 1.0 / alpha;
   for (int64_t m = 0; m < n; ++m) orc_doppler_one(n, W, fs, fc, beta, kb, x, m, y + 2 * m);
   return 0;
@@ -302,7 +308,7 @@ int orc_doppler_win(int64_t n, int W, double fs, double fc, double alpha, double
  * pulse would take too long); OpenMP over the samples. */
 int orc_doppler_at(int64_t n, int W, double fs, double fc, double alpha, double kb, const double *x,
                    int64_t nidx, const int64_t *idx, double *y) {
-  if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0)) return -1;
+  if (n < 1 || W < 1 || !(alpha > 0.0) || !(kb >= 0.0 || kb == ORC_HANN)) return -1;
   double beta = 1.0 / alpha;
   int err = 0;
 #ifdef _OPENMP

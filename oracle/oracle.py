@@ -67,6 +67,8 @@ def _load():
         lib.orc_bessel_i0.argtypes = [d]
         lib.orc_kaiser.restype = d
         lib.orc_kaiser.argtypes = [d, d, d]
+        lib.orc_hann.restype = d
+        lib.orc_hann.argtypes = [d, d]
         lib.orc_run_batch_win.restype = i32
         lib.orc_run_batch_win.argtypes = [i32, i64, i64, d, d, i32, d, p, p, p, p, i32, i32]
         lib.orc_pq_resample.restype = i32
@@ -189,6 +191,14 @@ def doppler_at(x, W: int, fs: float, fc: float, alpha: float, idx, kaiser: float
 def bessel_i0(z: float) -> float:
     """Modified Bessel function I0 by its power series (the taper's definition, R17)."""
     return _load().orc_bessel_i0(float(z))
+
+
+HANN = -1.0  # pass as `kaiser` to select the Hann taper (oracle.c ORC_HANN)
+
+
+def hann(d: float, L: float) -> float:
+    """Hann taper (1 + cos(pi d / L)) / 2 (R17)."""
+    return _load().orc_hann(float(d), float(L))
 
 
 def kaiser(d: float, L: float, kb: float) -> float:

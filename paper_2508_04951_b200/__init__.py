@@ -88,6 +88,7 @@ def load():
         "dc_doppler_pq": ([p, p, p, i64, pd], i32),
         "dc_set_reference": ([p, p, i64], i32),
         "dc_set_taper": ([p, d], i32),
+        "dc_set_window": ([p, i32, d], i32),
         "dc_compress": ([p, p, p, i64, pd], i32),
         "dc_correct": ([p, p, p, i64, pd, pd], i32),
         "dc_correct_host": ([p, p, p, i64, pd, pd], i32),
@@ -255,6 +256,13 @@ class Plan:
     def set_taper(self, kaiser: float = 0.0):
         """Kaiser taper (shape `kaiser`, 0 = rectangular) of the Doppler sinc window (reading R17)."""
         _check(load().dc_set_taper(self._h, float(kaiser)))
+        return self
+
+    WINDOWS = {"rect": 0, "kaiser": 1, "hann": 2}
+
+    def set_window(self, kind: str = "rect", param: float = 0.0):
+        """Window of the Doppler sinc taps: "rect", "kaiser" (shape `param`) or "hann" (reading R17)."""
+        _check(load().dc_set_window(self._h, self.WINDOWS[kind], float(param)))
         return self
 
     def set_reference(self, r):

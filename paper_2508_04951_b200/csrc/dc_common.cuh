@@ -32,7 +32,11 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
+#ifdef DC_NO_PDL  // diagnostics build: plain stream-ordered launches
+  cfg.numAttrs = 0;
+#else
   cfg.numAttrs = 1;
+#endif
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

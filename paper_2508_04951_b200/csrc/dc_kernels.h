@@ -75,10 +75,14 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &a, int pass, int var);
 // Kaiser taper of the sinc window (reading R17): K(d) = P(q), q = kb^2/4 (1 - (d/L)^2), L = W/2,
 // P(q) = sum_j q^j / ((j!)^2 I0(kb)) -- the I0 power series, normalised, truncated at kTaperTerms
 constexpr int kTaperTerms = 25;
+// Hann taper (reading R17): K(d) = (1 + cos(pi d / L)) / 2; selected by the taper code kTaperHann in place
+// of a Kaiser series length
+constexpr int kTaperHann = 1;
 struct TaperCoef {
   float c[kTaperTerms];  // c[j] = 1 / ((j!)^2 I0(kb)), FP32 (from binary64)
   float qa;              // kb^2 / 4
   float inv_L2;          // 1 / L^2
+  float pi_over_L;       // Hann: pi / L
 };
 
 struct DopplerArgs {
@@ -92,9 +96,9 @@ struct DopplerArgs {
   double carrier_cycles_per_sample;  // fc / fs; carrier phase psi_m = fc (1 - beta) m / fs
   cudaStream_t stream;
   int grid_cap;  // max CTAs of the persistent grid (0: one wave of the whole GPU)
-  bool taper;       // Kaiser taper on (coefficients in tc)
+  bool taper;       // taper on (coefficients in tc)
   TaperCoef tc;
-  int taper_terms;  // series terms needed (17 or kTaperTerms)
+  int taper_terms;  // Kaiser: series terms needed (17 or kTaperTerms); kTaperHann: the Hann window
   void *desc;       // plan-owned per-CTA tile-geometry slots (kDopDescBytes)
 };
 constexpr int kDopMaxCtas = 1024;                       // persistent Doppler grid cap

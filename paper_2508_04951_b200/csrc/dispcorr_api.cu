@@ -698,8 +698,22 @@ dc_status dc_set_reference(dc_plan_t p, const void *r, int64_t L) {
   return DC_OK;
 }
 
-dc_status dc_set_taper(dc_plan_t p, double kaiser) {
+dc_status dc_set_window(dc_plan_t p, int kind, double param) {
   if (!p) return fail(DC_ERR_NULL_POINTER, "plan is NULL");
+  if (kind == DC_WINDOW_RECT) {
+    p->taper = false;
+    p->kaiser = 0.0;
+    return DC_OK;
+  }
+  if (kind == DC_WINDOW_HANN) {
+    p->tc.pi_over_L = (float)(2.0 * dc::kPi / (double)p->taps);
+    p->taper_terms = dc::kTaperHann;
+    p->kaiser = 0.0;
+    p->taper = true;
+    return DC_OK;
+  }
+  if (kind != DC_WINDOW_KAISER) return fail(DC_ERR_INVALID_VALUE, "window kind %d unknown", kind);
+  const double kaiser = param;
   if (!std::isfinite(kaiser) || kaiser < 0.0 || kaiser > 12.0)
     return fail(DC_ERR_INVALID_VALUE, "kaiser = %g must be finite and in [0, 12]", kaiser);
   // I0(kb) and the normalised series coefficients 1 / ((j!)^2 I0(kb)) in binary64
@@ -725,6 +739,8 @@ dc_status dc_set_taper(dc_plan_t p, double kaiser) {
   p->taper = kaiser > 0.0;
   return DC_OK;
 }
+
+dc_status dc_set_taper(dc_plan_t p, double kaiser) { return dc_set_window(p, DC_WINDOW_KAISER, kaiser); }
 
 dc_status dc_compress(dc_plan_t p, const void *x, void *z, int64_t batch, const double *tec) {
   return iono_common(p, x, z, batch, tec, 2);

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
       float h = s / d;
       if constexpr (TAPER > 0) {
         float Kt, dKt;
-        kaiser_taper<TAPER>(tcoef, d, Kt, dKt);
+        taper_eval<TAPER>(tcoef, d, Kt, dKt);
         h *= Kt;
       }
       const float2 xv = __ldg(xp + k);
@@ -193,6 +193,7 @@ static cudaError_t launch_pipe_w(const DopplerArgs &a) {
 static cudaError_t launch_doppler_fast(const DopplerArgs &a, bool second) {
   if (a.taper) {
     if (second) return cudaErrorInvalidValue;
+    if (a.taper_terms == kTaperHann) return launch_pipe_w<false, kTaperHann>(a);
     return a.taper_terms <= 17 ? launch_pipe_w<false, 17>(a) : launch_pipe_w<false, kTaperTerms>(a);
   }
   return second ? launch_pipe_w<true>(a) : launch_pipe_w<false>(a);
@@ -200,8 +201,10 @@ static cudaError_t launch_doppler_fast(const DopplerArgs &a, bool second) {
 
 static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
   dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)a.pulses);
-  auto kern = !a.taper ? doppler_exact_kernel<0>
-                       : (a.taper_terms <= 17 ? doppler_exact_kernel<17> : doppler_exact_kernel<kTaperTerms>);
+  auto kern = !a.taper                         ? doppler_exact_kernel<0>
+              : a.taper_terms == kTaperHann ? doppler_exact_kernel<kTaperHann>
+              : a.taper_terms <= 17         ? doppler_exact_kernel<17>
+                                            : doppler_exact_kernel<kTaperTerms>;
   return launch_pdl(kern, grid, dim3(256), 0, a.stream, a.x, a.y, a.n, a.taps, a.pp, a.pulse_base,
                     a.carrier_cycles_per_sample, a.tc);
 }

@@ -96,6 +96,25 @@ __device__ __forceinline__ void kaiser_taper(const TaperCoef &tc, float d, float
   dK = db * (-2.0f * tc.qa * tc.inv_L2 * d);  // dP/dq * dq/dd
 }
 
+// Hann taper K(d) = (1 + cos(pi d / L)) / 2 and K'(d) = -(pi / 2L) sin(pi d / L), |d| <= L (reading R17):
+// SFU sin/cos of an argument in [-pi, pi] (absolute error ~4e-7, i.e. ~2e-7 in K)
+__device__ __forceinline__ void hann_taper(const TaperCoef &tc, float d, float &K, float &dK) {
+  float sn, cs;
+  __sincosf(d * tc.pi_over_L, &sn, &cs);
+  K = fmaf(0.5f, cs, 0.5f);
+  dK = -0.5f * tc.pi_over_L * sn;
+}
+
+// taper code TAPER: 0 none, kTaperHann, else a Kaiser series of TAPER terms
+template <int TAPER>
+__device__ __forceinline__ void taper_eval(const TaperCoef &tc, float d, float &K, float &dK) {
+  if constexpr (TAPER == kTaperHann) {
+    hann_taper(tc, d, K, dK);
+  } else {
+    kaiser_taper<TAPER>(tc, d, K, dK);
+  }
+}
+
 // Window membership of the thread's R outputs (reading R9, the oracle's roundings): output r owns the
 // union taps [a_r, a_r + W - 1], a_r in {0, 1}, a_r = 1 iff its window start K_r = floor(x_r) + 1
 // equals B + r + 1, i.e. iff x_r = fl(fl((mt + r) beta) - W/2) >= B + r (exact binary64 comparison:
@@ -120,8 +139,8 @@ __device__ __forceinline__ uint32_t dop_membership(double md, double beta, doubl
 // One doppler tile: R outputs per thread from the staged span sb (x[Bcta + i] = sb[i]), carrier
 // rotation, then the warp's R x 32 contiguous outputs leave through its shared-memory segment `ob`
 // (kDopSeg samples) as ONE bulk async copy issued by lane 0 (no LDS/STG per output, no CTA barrier).
-// TAPER > 0: Kaiser-tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only), with
-// TAPER series terms.
+// TAPER > 0: tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only): the Hann window
+// (TAPER == kTaperHann) or a Kaiser window of TAPER series terms.
 template <bool SECOND, int WT, int TAPER = 0>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
@@ -226,7 +245,7 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
     }
     if constexpr (TAPER > 0) {
       float K, dK;
-      kaiser_taper<TAPER>(*tcp, d, K, dK);
+      taper_eval<TAPER>(*tcp, d, K, dK);
       // the taper's centre weight is 1 exactly (R17): the FP32 Horner sum need not round to 1
       if (TINY && d == 0.f) K = 1.f;
       w1 = fmaf(w1, K, w * dK);

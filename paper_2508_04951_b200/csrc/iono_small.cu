@@ -1,0 +1,166 @@
+// iono_small.cu -- fused FFT -> ionospheric phase -> IFFT kernels (Eq. 15).
+//
+// Regime 0 (n <= 8192): one CTA holds whole pulses; forward FFT, phase and inverse FFT
+//   run back to back on registers + shared memory: one HBM read and one HBM write per
+//   sample (16 B / sample).
+// Regime 1 (n > 8192): four-step split n = N1 N2, t = N2 t1 + t2, k = k1 + N1 k2:
+//   pass A  column DFTs over t1 (N1 points) for each t2, times w_n^(k1 t2)        -> Z[k1][t2]
+//   pass B  row DFT over t2 (N2 points) -> bin k = k1 + N1 k2 -> phase (Eq. 15) ->
+//           inverse row DFT over k2, times w_n^(-k1 t2)                             -> Z'[k1][t2]
+//   pass C  inverse column DFTs over k1 -> y[N2 t1 + t2]
+//   Z and Z' live in the output buffer itself (in place); for dc_correct the output is a
+//   plan-owned chunk buffer sized to stay L2-resident, so HBM sees ~16 B / sample.
+// (this unit: single-CTA pulses n <= 8192, the pass plans and the four-step split)
+#include "iono_launch.cuh"
+
+namespace dc {
+
+template <int P, int VAR>
+static cudaError_t launch_small_pv(const TileArgs &a, cudaStream_t st, int cap) {
+  constexpr int NB = small_nb(P);
+  const int64_t total = (a.pulses + NB - 1) / NB;
+  return launch_tile_cfg<P, small_loge<P>(), NB, true, MODE_SMALL, VAR>(a, total, st, cap);
+}
+template <int P>
+static cudaError_t launch_small_p(const TileArgs &a, int var, cudaStream_t st, int cap) {
+  switch (var) {
+    case VAR_CORRECT: return launch_small_pv<P, VAR_CORRECT>(a, st, cap);
+    case VAR_DISTORT: return launch_small_pv<P, VAR_DISTORT>(a, st, cap);
+    case VAR_COMPRESS: return launch_small_pv<P, VAR_COMPRESS>(a, st, cap);
+    case VAR_REFERENCE: return launch_small_pv<P, VAR_REFERENCE>(a, st, cap);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int N1>
+static cudaError_t launch_wsmall(const WarpArgs &a, int var, cudaStream_t st, int cap) {
+  auto kern = (var == VAR_DISTORT) ? warp_small_kernel<N1, VAR_DISTORT> : warp_small_kernel<N1, VAR_CORRECT>;
+  const size_t smem = wsmall_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
+  int64_t grid = std::min<int64_t>(tiles, sms);
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWsT), smem, st, a);
+}
+
+cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
+  TileArgs a{};
+  a.src = s.xin;
+  a.dst = s.xout;
+  a.pulses = s.batch;
+  a.pulse_stride = (int64_t)1 << s.log2n;
+  a.pulse_base = 0;
+  a.log2n = s.log2n;
+  a.pp = s.pp;
+  a.twf = s.twf;
+  a.twi = s.twi;
+  a.H = 0;
+  a.fs_over_n = s.fs_over_n;
+  a.fc = s.fc;
+  a.ref = s.ref;
+  a.ref_idx = s.ref_idx;
+  a.ref_out = s.ref_out;
+  if (s.log2n == 10 && s.tw1024 && s.gtab)
+    return launch_warp_row<MODE_SMALL>(warp_args(a, s.tw1024, s.gtab), var, s.stream, s.grid_cap);
+  // in-CTA four-step on the warp FFT (wsmall.cuh) for 4096 / 8192: +5 % / +18 % over the tile
+  // kernel; for 2048 the tile kernel is faster (128 vs 148 GS/s measured) and stays.  Pulse
+  // compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).
+  if (s.log2n >= 12 && s.log2n <= 13 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
+    const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
+    return (s.log2n == 12) ? launch_wsmall<4>(w, var, s.stream, s.grid_cap) : launch_wsmall<8>(w, var, s.stream, s.grid_cap);
+  }
+  switch (s.log2n) {
+    case 1: return launch_small_p<1>(a, var, s.stream, s.grid_cap);
+    case 2: return launch_small_p<2>(a, var, s.stream, s.grid_cap);
+    case 3: return launch_small_p<3>(a, var, s.stream, s.grid_cap);
+    case 4: return launch_small_p<4>(a, var, s.stream, s.grid_cap);
+    case 5: return launch_small_p<5>(a, var, s.stream, s.grid_cap);
+    case 6: return launch_small_p<6>(a, var, s.stream, s.grid_cap);
+    case 7: return launch_small_p<7>(a, var, s.stream, s.grid_cap);
+    case 8: return launch_small_p<8>(a, var, s.stream, s.grid_cap);
+    case 9: return launch_small_p<9>(a, var, s.stream, s.grid_cap);
+    case 10: return launch_small_p<10>(a, var, s.stream, s.grid_cap);
+    case 11: return launch_small_p<11>(a, var, s.stream, s.grid_cap);
+    case 12: return launch_small_p<12>(a, var, s.stream, s.grid_cap);
+    case 13: return launch_small_p<13>(a, var, s.stream, s.grid_cap);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Pass plans (radix sequences) exported to the host so it can build the twiddle tables.
+template <int P, int LOGR>
+static void fill_plan(PlanDesc &d) {
+  using PP = PassPlan<P, LOGR>;
+  d.npass = PP::npass;
+  for (int i = 0; i < PP::npass; ++i) {
+    d.log_radix_fwd[i] = PP::log_radix_fwd(i);
+    d.log_radix_inv[i] = PP::log_radix_inv(i);
+    d.log_ns_fwd[i] = PP::log_ns_fwd(i);
+    d.log_ns_inv[i] = PP::log_ns_inv(i);
+    d.tw_off_fwd[i] = PP::tw_off_fwd(i);
+    d.tw_off_inv[i] = PP::tw_off_inv(i);
+  }
+  d.tw_size = PP::tw_size();
+}
+
+template <int P>
+static void fill_small(PlanDesc &d) { fill_plan<P, small_loge<P>()>(d); }
+
+bool describe_small_plan(int P, PlanDesc &d) {
+  switch (P) {
+    case 1: fill_small<1>(d); return true;
+    case 2: fill_small<2>(d); return true;
+    case 3: fill_small<3>(d); return true;
+    case 4: fill_small<4>(d); return true;
+    case 5: fill_small<5>(d); return true;
+    case 6: fill_small<6>(d); return true;
+    case 7: fill_small<7>(d); return true;
+    case 8: fill_small<8>(d); return true;
+    case 9: fill_small<9>(d); return true;
+    case 10: fill_small<10>(d); return true;
+    case 11: fill_small<11>(d); return true;
+    case 12: fill_small<12>(d); return true;
+    case 13: fill_small<13>(d); return true;
+    default: return false;
+  }
+}
+
+bool describe_fourstep_plan(int P, PlanDesc &d) {
+  switch (P) {
+    case 7: fill_plan<7, DC_FS_LOGE>(d); return true;
+    case 8: fill_plan<8, DC_FS_LOGE>(d); return true;
+    case 9: fill_plan<9, DC_FS_LOGE>(d); return true;
+    case 10: fill_plan<10, DC_FS_LOGE>(d); return true;
+    case 11: fill_plan<11, DC_FS_LOGE>(d); return true;
+    case 12: fill_plan<12, DC_FS_LOGE>(d); return true;
+    case 13: fill_plan<13, DC_FS_LOGE>(d); return true;
+    default: return false;
+  }
+}
+
+void fourstep_split(int log2n, int &P1, int &P2) {
+  if (log2n == 22 || log2n == 23) {  // warp column passes (N1 = 1024) + tile row pass (N2 = 2^12, 2^13):
+    P1 = 10;                         // 63 vs 47 GS/s at 2^22 over the tile-only split
+    P2 = log2n - 10;
+    return;
+  }
+  // row pass on the warp-level 1024-point FFT; 2^14 .. 2^16: columns of N1 = 16 .. 64 on the
+  // thread-per-column kernel (tcol.cuh)
+  if (log2n >= 14 && log2n <= 21) {
+    P2 = 10;
+    P1 = log2n - 10;
+    return;
+  }
+  P2 = (log2n + 1) / 2;
+  if (log2n - P2 > 11) P2 = log2n - 11;
+  if (P2 > 13) P2 = 13;
+  P1 = log2n - P2;
+}
+
+int tw1024_offset() { return kTw1024Off; }
+
+}  // namespace dc

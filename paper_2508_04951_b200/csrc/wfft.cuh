@@ -96,6 +96,7 @@ struct WarpArgs {
   const float2 *ref;   // VAR_COMPRESS: T = conj(R_k) tables (n entries each, same layout as gtab)
   const int *ref_idx;  // VAR_COMPRESS: per-pulse table index (indexed like pp), or null = table 0
   float2 *ref_out;     // VAR_REFERENCE: conj(X_k) per pulse (n entries each, same layout as gtab)
+  int outer_c;         // the conj outer twiddle of pass B is applied by pass C on load (n = 2^20: both warp-level)
 };
 
 // (RowVar: what the row kernel does between its forward and inverse DFTs -- tile_fft.cuh)
@@ -248,7 +249,11 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
 
     // ---- outputs t2 = lane + 32 s: conj outer twiddle (ROWB) and coalesced stores
     float2 *out = const_cast<float2 *>(row_ptr(a.dst, it));
-    if constexpr (MODE == MODE_ROWB) {
+    if (MODE == MODE_ROWB && a.outer_c) {
+      // the compute-bound row pass leaves the conj outer twiddle to the memory-bound pass C
+#pragma unroll
+      for (int s = 0; s < 32; ++s) __stcg(out + lane + 32 * s, v[s]);
+    } else if constexpr (MODE == MODE_ROWB) {
       __syncwarp();
       Pw[lane] = twn((32u * k1 * (uint32_t)lane) & nmask, log2n);
       const float2 base = twn((k1 * (uint32_t)lane) & nmask, log2n);
@@ -349,6 +354,16 @@ __global__ void __launch_bounds__(2 * kWW * 32, 1) warp_col3_kernel(const WarpAr
 #pragma unroll
       for (int s = 0; s < 32; ++s) v[s] = cmul(v[s], cmul(base, Pw[s]));
     } else {
+      if (a.outer_c) {
+        // pass B's conj outer twiddle w_n^(-k1 t2) on the inputs k1 = lane + 32 r of column t2
+        const uint32_t t2 = (uint32_t)(c0 + warp);
+        __syncwarp();
+        Pw[lane] = twn((32u * t2 * (uint32_t)lane) & nmask, log2n);
+        const float2 base = twn((t2 * (uint32_t)lane) & nmask, log2n);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = cmulc(v[r], cmul(base, Pw[r]));
+      }
       wfft1024<true>(v, wk, Tw, lane);
     }
     __syncwarp();

@@ -280,7 +280,7 @@ def test_abi_errors_on_gpu(dc):
 
 # ----------------------------------------------------------------------------- pulse compression (NEXT-2)
 def gpu_compress(dc, x, r, fs, fc, tec, inplace=False):
-    p = dc.Plan(x.shape[-1], fs, fc, taps=8)
+    p = dc.Plan(x.shape[-1], fs, fc, taps=min(8, x.shape[-1]))
     p.set_reference(to_dev(r))
     t = to_dev(x)
     z = t if inplace else to_dev(np.zeros_like(x))
@@ -368,6 +368,50 @@ def test_doppler_kaiser_vs_oracle(dc, case, W, kb):
         ref = O.run_batch("doppler", x, fs, fc, W, None, alphas, kaiser=kb)
         err = rel_l2(y, ref)
         assert err.max() < TOL, (case, W, kb, fs, fc, err.max())
+
+
+def gpu_doppler_window(dc, x, W, fs, fc, alpha, kind, param=0.0):
+    import torch
+    p = dc.Plan(x.shape[-1], fs, fc, taps=W)
+    p.set_window(kind, param)
+    t = to_dev(x)
+    y = torch.empty_like(t)
+    p.doppler(t, y, alpha)
+    return from_dev(y)
+
+
+@pytest.mark.parametrize("case", ["fast1", "fast2", "exact"])
+@pytest.mark.parametrize("W", [8, 16, 25, 32, 64, 128, 7])
+def test_doppler_hann_vs_oracle(dc, case, W):
+    # Hann taper (R17): first-order fast path, the second-order drift range (tapered: exact path) and the
+    # exact-tap kernel; compile-time and runtime W
+    n = 4096
+    alphas = np.array(ALPHA_CASES[case])
+    x = synth.complex_gaussian(n, seed=W + 17, batch=len(alphas)).astype(np.complex64)
+    for fs, fc in ((2.048e9, 0.0), (51.2e6, 422e6)):
+        y = gpu_doppler_window(dc, x, W, fs, fc, alphas, "hann")
+        ref = O.run_batch("doppler", x, fs, fc, W, None, alphas, kaiser=O.HANN)
+        assert rel_l2(y, ref).max() < TOL, (case, W, fs, fc)
+
+
+def test_doppler_hann_alpha_one_bit_exact_and_window_switch(dc):
+    import torch
+    x = synth.complex_gaussian(8192, seed=5, batch=2).astype(np.complex64)
+    assert np.array_equal(gpu_doppler_window(dc, x, 32, 51.2e6, 422e6, [1.0, 1.0], "hann"), x)
+    # switching windows on one plan: hann -> rect -> kaiser reproduce the oracle of each
+    p = dc.Plan(8192, 2.048e9, 0.0, taps=16)
+    xd = to_dev(x)
+    a = [1 + 2e-5, 1 - 3e-5]
+    for kind, param, kb in (("hann", 0.0, O.HANN), ("rect", 0.0, 0.0), ("kaiser", 6.0, 6.0)):
+        p.set_window(kind, param)
+        yd = torch.empty_like(xd)
+        p.doppler(xd, yd, a)
+        ref = O.run_batch("doppler", x, 2.048e9, 0.0, 16, None, a, kaiser=kb)
+        assert rel_l2(from_dev(yd), ref).max() < TOL, kind
+    with pytest.raises(dc.DispCorrError):
+        dc.load()
+        import ctypes
+        dc._check(dc.load().dc_set_window(p._h, 7, 0.0))
 
 
 def test_doppler_kaiser_second_order_drift_takes_exact_path(dc):

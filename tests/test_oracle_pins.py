@@ -612,3 +612,30 @@ def test_doppler_pq_at_matches_full_with_carrier(n, M):
     full = O.doppler_pq(x, fs, fc, alpha)[idx]
     at = O.doppler_pq_at(x, fs, fc, alpha, idx)
     assert np.abs(at - full).max() < 1e-12 * np.abs(full).max()
+
+
+# ----------------------------------------------------------------------------- Hann taper (R17, NEXT-3)
+def test_hann_taper_shape():
+    L = 16.0
+    assert O.hann(0.0, L) == 1.0                              # centre tap untouched: alpha = 1 stays exact
+    assert abs(O.hann(L, L)) < 1e-16 and abs(O.hann(-L, L)) < 1e-16   # zero at the window edges
+    assert abs(O.hann(L / 2, L) - 0.5) < 1e-15               # cos^2(pi/4)
+    for d in (0.3, 2.5, 7.0, 15.9):
+        assert O.hann(d, L) == O.hann(-d, L)
+        assert abs(O.hann(d, L) - np.cos(np.pi * d / (2 * L)) ** 2) < 1e-15   # cos^2(pi d / 2L) identity
+
+
+def test_hann_alpha_one_identity_and_accuracy():
+    x = synth.complex_gaussian(512, seed=3)
+    assert np.array_equal(O.doppler(x, 32, 1e6, 0.0, 1.0, kaiser=O.HANN), x)
+    # dilated Tukey LFM (as the Kaiser pin): the Hann taper beats the rectangular window at W = 32
+    n, fs = 1 << 14, 2.048e9
+    T = 0.8 * n / fs
+    alpha = O.alpha_from_velocity(5000.0)
+    t = np.arange(n) / fs
+    truth = _tukey_at(t - (n // 10) / fs, T)
+    echo = _tukey_at(alpha * t - (n // 10) / fs, T)
+    nrm = np.linalg.norm(truth)
+    err = lambda W, kb: np.linalg.norm(O.doppler(echo, W, fs, 0.0, alpha, kaiser=kb) - truth) / nrm
+    rect32, h32 = err(32, 0.0), err(32, O.HANN)
+    assert h32 < rect32 / 5

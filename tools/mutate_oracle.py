@@ -37,6 +37,10 @@ MUTANTS = {
     "pq no carrier": ("double psi = fc * (1.0 - beta_eff) * (double)m / fs;", "double psi = 0.0 * fc * (1.0 - beta_eff) * (double)m / fs;"),
     "exact carrier sign": ("    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---", "    double ang = 2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---"),
     "exact no carrier": ("    double psi = fc * (1.0 - beta) * (double)m / fs;\n    double r = psi - nearbyint(psi);\n    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---", "    double psi = 0.0;\n    double r = psi - nearbyint(psi);\n    double ang = -2.0 * ORC_PI * r;\n    double c = cos(ang), s = sin(ang);\n    y[2 * m] = re * c - im * s;\n    y[2 * m + 1] = re * s + im * c;\n  }\n  return 0;\n}\n\n/* ---"),
+    "pq_at inverse length n": ("const int64_t km = (int64_t)(((__int128)k * m) % M);", "const int64_t km = (int64_t)(((__int128)k * m) % n);"),
+    "pq_at forward sign": ("  memcpy(X, x, sizeof(double) * 2 * (size_t)n);\n  orc_fft(n, X, -1);", "  memcpy(X, x, sizeof(double) * 2 * (size_t)n);\n  orc_fft(n, X, +1);"),
+    "hann half-width W": ("double orc_hann(double d, double L) { return 0.5 * (1.0 + cos(ORC_PI * d / L)); }", "double orc_hann(double d, double L) { return 0.5 * (1.0 + cos(ORC_PI * d / (2.0 * L))); }"),
+    "hann not halved": ("double orc_hann(double d, double L) { return 0.5 * (1.0 + cos(ORC_PI * d / L)); }", "double orc_hann(double d, double L) { return (1.0 + cos(ORC_PI * d / L)); }"),
 }
 
 failed_to_catch = []
