@@ -316,6 +316,28 @@ def main():
         hit = [v for k, v in per.items() if kname in k]
         if hit:
             traffic = hit[0] * kern[dom]["samples_per_launch"]
+    # counter-based FP32 ceilings (tools/ncu_fp32_ops.py on the committed ncu --set full capture): executed
+    # FFMA/FADD/FMUL lane-operations per sample (packed x2 ops count twice) -> 148 x 128 lanes x clock / ops
+    ofiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fp32_ops.json")))
+    if ofiles and n == (1 << 20):
+        ops = json.load(open(ofiles[-1]))
+        lanes = 148 * 128 * sm_max * 1e6
+
+        def lane_ops(frag):
+            hit = [v["fp32_lane_ops_per_sample"] for k, v in ops.items() if frag in k]
+            return hit[0] if hit else None
+        if fft_stage is not None and "fft_stage" in ops:
+            per = ops["fft_stage"]["fp32_lane_ops_per_sample"]
+            ceil = min(lanes / per, hbm * 1e9 / 16.0)
+            fft_stage.update({"fp32_lane_ops_per_sample": per, "fp32_pipe_ceiling_samples_per_s": lanes / per,
+                              "ceiling_samples_per_s": ceil, "frac_of_ceiling": fft_stage["samples_per_s"] / ceil,
+                              "ceiling": "min(HBM at 16 B/sample, FP32 pipe at the counted lane-ops)",
+                              "counters": os.path.relpath(ofiles[-1], ROOT)})
+        per_d = lane_ops("doppler_pipe_kernel<0, 32, 0>")
+        if per_d and "doppler" in kern:
+            sps = kern["doppler"]["samples_per_launch"] / (kern["doppler"]["ms_per_launch"] / 1e3)
+            kern["doppler"].update({"fp32_lane_ops_per_sample": per_d, "fp32_pipe_ceiling_samples_per_s": lanes / per_d,
+                                    "frac_fp32_pipe_counted": sps * per_d / lanes})
     roofline = {"bound": "hbm", "achieved": kern[dom]["gbs"], "peak": hbm, "unit": "GB/s",
                 "frac": kern[dom]["gbs"] / hbm, "traffic": traffic, "kernel": dom, "peak_source": peak_kind,
                 "bytes_per_sample": 16, "algorithmic_bytes_per_launch": 16 * kern[dom]["samples_per_launch"],

@@ -30,11 +30,15 @@
 
 namespace dc {
 
-// Persistent pipeline over kDopBufs input buffers: thread 0 (the producer) stages tile i + 1 with the
-// TMA engine while the CTA computes tile i; each buffer has a `full` transaction mbarrier (TMA bytes)
-// and an `empty` mbarrier (one arrival per consumer warp once its lanes have read the buffer), so warps
-// run up to one tile apart with no CTA-wide barrier.  The tile geometry reaches the consumers through the
-// TMA engine too (from a per-CTA global slot), counted by the same `full` barrier as the data.
+// Persistent pipeline over kDopBufs input buffers: buffer b holds local tiles b, b + kDopBufs, ...; each
+// has a `full` transaction mbarrier (TMA bytes) and a release counter.  A warp that has finished reading
+// buffer b counts itself out; the LAST warp to do so restages the buffer with tile i + kDopBufs right
+// away, so the load is issued as early as possible (kDopBufs - 1 tiles of compute ahead of its first
+// consumer) and no warp ever blocks on a slower one -- warps run up to kDopBufs - 1 tiles apart with no
+// CTA-wide barrier.  (The previous design had thread 0 wait on an `empty` barrier before staging tile
+// i + 1, which stalled warp 0 -- and with it the prefetch -- behind the slowest warp.)  The tile geometry
+// reaches the consumers through the TMA engine too (from a per-CTA global slot), counted by the same
+// `full` barrier as the data.
 // WT > 0: the tap count W is a compile-time constant (fully unrolled tap loop); WT = 0: runtime W.
 #ifndef DC_DOP_MINB
 #define DC_DOP_MINB 2
@@ -53,16 +57,15 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
   DopTile *tiles = reinterpret_cast<DopTile *>(ob + kDopM);
   auto dslot = [&](int b) { return reinterpret_cast<DopTile *>(reinterpret_cast<char *>(tiles) + 128 * b); };
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(tiles) + 128 * kDopBufs);  // TMA completion
-  uint64_t *empty = full + kDopBufs;                                 // consumer-warp release per buffer
+  uint32_t *released = reinterpret_cast<uint32_t *>(full + kDopBufs);  // warps done with each buffer
   const int W = (WT > 0) ? WT : W_rt;
   const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t tiles_per_pulse = (uint32_t)((n + kDopM - 1) / kDopM);
   const uint32_t total = (uint32_t)pulses * tiles_per_pulse;
   if (blockIdx.x >= total) return;
   const uint32_t my_tiles = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  auto produce = [&](uint32_t i) {  // thread 0: stage local tile i into buffer i % kDopBufs
+  auto produce = [&](uint32_t i) {  // one thread: stage local tile i into buffer i % kDopBufs (free)
     const int b = (int)(i % kDopBufs);
-    if (i >= (uint32_t)kDopBufs) mbar_wait(&empty[b], ((i / kDopBufs) - 1) & 1u);  // tile i - kDopBufs released
     const uint32_t it = blockIdx.x + i * gridDim.x;
     const DopTile t = dop_tile(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
     const int slot = (int)blockIdx.x * kDopBufs + b;
@@ -71,21 +74,32 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
   if (tid == 0) {
     for (int b = 0; b < kDopBufs; ++b) {
       mbar_init(&full[b], 1);
-      mbar_init(&empty[b], kDopT / 32);
+      released[b] = 0u;
     }
     mbar_fence_init();
-    produce(0);
+    for (uint32_t i = 0; i < (uint32_t)kDopBufs && i < my_tiles; ++i) produce(i);
   }
   __syncthreads();
   float2 *obw = ob + (tid >> 5) * kDopSeg;
   for (uint32_t i = 0; i < my_tiles; ++i) {
-    if (tid == 0 && i + 1 < my_tiles) produce(i + 1);
     const int b = (int)(i % kDopBufs);
     mbar_wait(&full[b], (i / kDopBufs) & 1u);
     const DopTile cur = *dslot(b);
-    dop_tile_compute<SECOND, WT, TAPER>(xs + b * buf_elems, cur, W, obw, y, n, carrier, &tc);
+    // a pulse's last tile is ragged: warps whose outputs all lie past n skip it (their issue slots go to
+    // the other CTA of the SM), so short pulses waste at most one warp segment instead of a tile
+    if (cur.m0 + (int64_t)(tid >> 5) * kDopSeg < n)
+      dop_tile_compute<SECOND, WT, TAPER>(xs + b * buf_elems, cur, W, obw, y, n, carrier, &tc);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done reading buffer b
+    if (lane == 0) {
+      // this warp's reads of buffer b are done (release); the last warp out acquires and restages it.
+      // Nobody else touches released[b] until tile i + kDopBufs -- the one staged here -- is consumed.
+      __threadfence_block();
+      if (atomicAdd(&released[b], 1u) == (uint32_t)(kDopT / 32 - 1)) {
+        released[b] = 0u;
+        __threadfence_block();
+        if (i + kDopBufs < my_tiles) produce(i + kDopBufs);
+      }
+    }
   }
   if (lane == 0) bulk_store_wait_all();  // the warp's last output segment has left shared memory
 }
@@ -147,7 +161,7 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
   const int span = (int)(kDopM * (1.0 + kDopMaxDrift)) + a.taps + kDopR + 16;
   const int buf = (span + kDopBox - 1) / kDopBox * kDopBox;  // whole TMA boxes
-  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + kDopM) + kDopBufs * (128 + 2 * sizeof(uint64_t)) + 1024;
+  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + kDopM) + kDopBufs * (128 + sizeof(uint64_t) + 4) + 1024;
   CUtensorMap xmap;
   {
     const uint64_t dims[2] = {(uint64_t)a.n, (uint64_t)a.pulses};

@@ -20,7 +20,7 @@ constexpr double kDopMaxDrift = 2.0e-3;  // max |beta - 1| * R / 2 for the fast 
 #ifndef DC_DOP_NBUF
 #define DC_DOP_NBUF 3
 #endif
-constexpr int kDopBufs = DC_DOP_NBUF;    // input staging buffers (prefetch distance 1: warps may lag one tile)
+constexpr int kDopBufs = DC_DOP_NBUF;    // input staging buffers (tile i + kDopBufs is staged once tile i is read)
 static_assert(kDopSeg % 2 == 0, "warp segments must be 16-byte multiples");
 
 __device__ __forceinline__ float frcp(float x) {
@@ -167,15 +167,21 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
 #pragma unroll
   for (int h = 0; h < kDopR / 2; ++h) dl[h] = make_float2((2 * h - RC) * db, (2 * h + 1 - RC) * db);
   const float dlast = (kDopR - 1 - RC) * db;  // the unpaired last output (odd R)
-  // reference position inside the union, split into nearest integer + fraction in [-1/2, 1/2]
-  const double vref = (md + (double)RC) * beta - (Bd + (double)RC);
-  const double ic_d = rint(vref);
-  const int ic = (int)ic_d;
-  const float u = __double2float_rn(vref - ic_d);
+  // Reference position (output RC) relative to the union's middle tap Mi = floor(W/2): vrel lies in
+  // (-1.0002, 1.5002), so the sample nearest to it is union tap Mi + k0, k0 = rint(vrel) in {-1, .., 2}.
+  // Union tap jj = Mi + k sits at distance d_k = vrel - k.  Taps k != k0 (|d| >= 1/2) take d = uf - k, one
+  // FADD with a compile-time k from the FP32 vrel (absolute error <= 2^-24: relative <= 2^-23); the nearest
+  // tap takes its weights from u = vrel - k0 rounded from binary64 (full relative precision next to the
+  // sample) by the series below -- so the tap loop has a single code path (no per-warp "tiny u" branch).
+  const int Mi = W >> 1;
+  const double vrel = (md + (double)RC) * beta - (Bd + (double)(RC + Mi));
+  const double k0d = rint(vrel);
+  const int k0 = (int)k0d;
+  const float u = __double2float_rn(vrel - k0d);
+  const float uf = __double2float_rn(vrel);
   float S, Cc;
   sincospif(u, &S, &Cc);
   S *= 0.31830988618379067f;  // sin(pi u) / pi
-  // centre-tap weights (d = u): series near 0 (sinc even; avoids C/d - S/(pi d^2) cancellation)
   float wc, w1c, w2c;
   {
     const float pd2 = 9.8696044010893586f * u * u;
@@ -190,19 +196,11 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       w2c = fmaf(-9.8696044010893586f, wc, -2.f * w1c * inv);
     }
   }
-  // the generic formula is exact enough except at the centre tap when |u| is tiny; decide per warp
-  const bool tiny = __any_sync(0xffffffffu, fabsf(u) < 1.0e-3f);
   const float2 *xb = sb + (B - cur.Bcta);  // x[B + i] = xb[i]
-  // sign of tap jj: (-1)^(jj - ic); fold (-1)^ic into the per-thread constants
-  const float Sp = (ic & 1) ? -S : S, Cp = (ic & 1) ? -Cc : Cc;
-  // distance of union tap jj from the reference position: d = u - (jj - ic), the integer part exact
-  // and one rounding (a running d -= 1 from u + ic would lose u's low bits near the centre tap)
-  const float icf = (float)ic;
+  const float Sp = (k0 & 1) ? -S : S, Cp = (k0 & 1) ? -Cc : Cc;
   float2 acc[kDopR];
 #pragma unroll
   for (int r = 0; r < kDopR; ++r) acc[r] = make_float2(0.f, 0.f);
-
-  // EDGE = 0: interior tap (all R outputs); 1: union tap 0 (outputs with a_r = 0); 2: union tap W (a_r = 1)
   auto mac = [&](const float2 *xv, float w, float w1, float w2, auto EDGEc) {
     constexpr int EDGE = decltype(EDGEc)::value;
     auto keep = [&](int r) { return EDGE == 0 || (((own1 >> r) & 1u) == (EDGE == 2 ? 1u : 0u)); };
@@ -228,48 +226,45 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       acc[kDopR - 1] = __ffma2_rn(xv[kDopR - 1], make_float2(hl, hl), acc[kDopR - 1]);
     }
   };
-  // weights of union tap jj at distance d = u - (jj - ic):
-  // sinc = (-1)^(jj-ic) S / d, sinc' = ((-1)^(jj-ic) C - sinc) / d, sinc'' = -pi^2 sinc - 2 sinc'/d.
-  // TINY: override the centre tap (jj == ic) with its series values.
-  auto weights = [&](int jj, float d, auto TINYc, float &w, float &w1, float &w2) {
-    constexpr bool TINY = decltype(TINYc)::value;
+  // weights of union tap jj = Mi + k at distance d: sinc = (-1)^k Sp / d, sinc' = ((-1)^k Cp - sinc) / d,
+  // sinc'' = -pi^2 sinc - 2 sinc'/d; the nearest tap (k == k0, possible only for k in [-1, 2]) takes wc, w1c, w2c
+  auto weights = [&](int k, float d, float &w, float &w1, float &w2) {
     const float inv = frcp(d);
-    const float s = (jj & 1) ? -Sp : Sp, c = (jj & 1) ? -Cp : Cp;
+    const float s = (k & 1) ? -Sp : Sp, c = (k & 1) ? -Cp : Cp;
     w = s * inv;
     w1 = inv * (c - w);
     w2 = SECOND ? fmaf(-9.8696044010893586f, w, -2.f * w1 * inv) : 0.f;
-    if (TINY && jj == ic) {
+    const bool near = (WT == 0 || (k >= -1 && k <= 2)) && k == k0;
+    if (near) {
       w = wc;
       w1 = w1c;
       w2 = w2c;
     }
     if constexpr (TAPER > 0) {
       float K, dK;
-      taper_eval<TAPER>(*tcp, d, K, dK);
-      // the taper's centre weight is 1 exactly (R17): the FP32 Horner sum need not round to 1
-      if (TINY && d == 0.f) K = 1.f;
+      taper_eval<TAPER>(*tcp, near ? u : d, K, dK);
+      if (near && u == 0.f) K = 1.f;
       w1 = fmaf(w1, K, w * dK);
       w *= K;
     }
   };
-  auto taps = [&](auto TINYc) {
-    // register window xw[r] = x[B + jj + r]; union taps jj = 0 .. W
+  // distance of union tap Mi + k
+  auto dist = [&](int k) { return ((WT == 0 || (k >= -1 && k <= 2)) && k == k0) ? u : uf - (float)k; };
+  {
     float2 xw[kDopR];
 #pragma unroll
     for (int r = 0; r < kDopR; ++r) xw[r] = xb[r];
     {
-      const float d = u + icf;
       float w, w1, w2;
-      weights(0, d, TINYc, w, w1, w2);
+      weights(-Mi, dist(-Mi), w, w1, w2);
       mac(xw, w, w1, w2, std::integral_constant<int, 1>());
     }
-    auto step = [&](int jj) {  // slide the window to tap jj and apply it (interior taps)
+    auto step = [&](int jj) {
 #pragma unroll
       for (int r = 0; r < kDopR - 1; ++r) xw[r] = xw[r + 1];
       xw[kDopR - 1] = xb[jj + kDopR - 1];
-      const float d = u - ((float)jj - icf);
       float w, w1, w2;
-      weights(jj, d, TINYc, w, w1, w2);
+      weights(jj - Mi, dist(jj - Mi), w, w1, w2);
       mac(xw, w, w1, w2, std::integral_constant<int, 0>());
     };
     if constexpr (WT > 0) {
@@ -283,16 +278,10 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
 #pragma unroll
       for (int r = 0; r < kDopR - 1; ++r) xw[r] = xw[r + 1];
       xw[kDopR - 1] = xb[W + kDopR - 1];
-      const float d = u - ((float)W - icf);
       float w, w1, w2;
-      weights(W, d, TINYc, w, w1, w2);
+      weights(W - Mi, dist(W - Mi), w, w1, w2);
       mac(xw, w, w1, w2, std::integral_constant<int, 2>());
     }
-  };
-  if (tiny) {
-    taps(std::true_type());
-  } else {
-    taps(std::false_type());
   }
 
   // ---- carrier rotation (reading R10)

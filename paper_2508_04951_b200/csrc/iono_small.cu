@@ -8,8 +8,10 @@
 //   pass B  row DFT over t2 (N2 points) -> bin k = k1 + N1 k2 -> phase (Eq. 15) ->
 //           inverse row DFT over k2, times w_n^(-k1 t2)                             -> Z'[k1][t2]
 //   pass C  inverse column DFTs over k1 -> y[N2 t1 + t2]
-//   Z and Z' live in the output buffer itself (in place); for dc_correct the output is a
-//   plan-owned chunk buffer sized to stay L2-resident, so HBM sees ~16 B / sample.
+//   (n = 2^20: the conj outer twiddle of pass B is applied by pass C on load instead.)
+//   Z and Z' live in the output buffer itself (in place); for dc_correct the output is the
+//   plan-owned launch-group buffer (2 GiB groups), so each pass streams ~16 B / sample through HBM
+//   (48 B / sample for the stage; ncu: profiles/r1b_ncu_full_summary.md).
 // (this unit: single-CTA pulses n <= 8192, the pass plans and the four-step split)
 #include "iono_launch.cuh"
 

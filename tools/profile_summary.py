@@ -28,7 +28,7 @@ stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_
 traffic = {}
 md = [f"# {tag} ncu --set full summaries (1 B200, --clock-control none)", "",
       f"Capture: `ncu --set full --import-source on --clock-control none -k regex:<kernels> -s 4 -c 4 -o ... "
-      f"python tools/debug/profile_driver.py 20 256 2` (256 pulses x 2^20 per launch group: {spl:,} samples per launch; "
+      f"python tools/profile_driver.py 20 256 2` (256 pulses x 2^20 per launch group: {spl:,} samples per launch; "
       f"algorithmic bytes = 16 B/sample = {16 * spl / 1e6:.1f} MB per launch).", ""]
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
@@ -65,7 +65,7 @@ for r in rows[hi + 1:]:
     ms = v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(r[ui], 1e-6)
     tot[name] += ms
     cnt[name] += 1
-default = {k: v for k, v in tot.items() if "fused" not in k and "at::" not in k}
+default = {k: v for k, v in tot.items() if "at::" not in k}
 T = sum(default.values())
 md = [f"# {tag} ncu launch list (C4: 1024 x 2^20 pulse train, dc_correct, 1 B200)", "",
       "Command (under gpurun): `ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ... "
