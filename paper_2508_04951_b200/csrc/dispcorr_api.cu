@@ -427,6 +427,28 @@ dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
   return DC_OK;
 }
 
+// dc_correct of one launch group: the fused single-round-trip kernel where it exists (single-CTA pulses,
+// n = 2^11 .. 2^13, W in {16, 32}, rectangular window, first/second-order Doppler path; NEXT-1), else
+// the ionospheric stage into the group buffer followed by the Doppler stage
+bool correct_fused_ok(const dc_plan_s *p, double max_abs_beta_m1) {
+  const int path = dc::doppler_path(max_abs_beta_m1, p->taper);
+  return p->regime == 0 && !p->taper && path != 0 && dc::correct_small_supported(p->log2n, p->taps);
+}
+dc_status run_correct(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
+                      int64_t pulse_base, double max_abs_beta_m1, Lane ln) {
+  if (correct_fused_ok(p, max_abs_beta_m1)) {
+    dc::IonoSmallArgs a{src, nullptr, pulses, p->log2n, pp + pulse_base, p->tw_small_f, p->tw_small_i,
+                        p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab, nullptr, nullptr, nullptr};
+    ProfScope ps(p, DC_K_CORRECT_FUSED, pulses * p->n, ln.st);
+    DC_CUDA(dc::launch_correct_small(a, dst, p->fc / p->fs, p->taps, dc::doppler_path(max_abs_beta_m1) == 2),
+            "fused dc_correct kernel launch");
+    return DC_OK;
+  }
+  dc_status s = run_iono(p, src, p->scratch, pulses, pp, pulse_base, 0, ln);
+  if (s == DC_OK) s = run_doppler(p, p->scratch, dst, pulses, pp, pulse_base, max_abs_beta_m1, ln);
+  return s;
+}
+
 // launch-group buffer for dc_correct: min(chunk, batch) pulses
 dc_status ensure_scratch(dc_plan_s *p, int64_t batch) {
   const int64_t need = std::min(p->chunk, batch) * p->n * (int64_t)sizeof(float2);
@@ -829,11 +851,12 @@ dc_status dc_doppler_pq(dc_plan_t p, const void *x, void *y, int64_t batch, cons
   struct Group {
     int64_t b0, nb;
     std::vector<std::pair<int, int64_t>> builds;  // (slot, M) tables to build before the group
+    bool identity;                                // all pulses of the group have M == n
   };
   std::vector<Group> groups;
   int *slot_h = p->pq_host, *M_h = p->pq_host + batch;
   for (int64_t b0 = 0; b0 < batch;) {
-    Group g{b0, 0, {}};
+    Group g{b0, 0, {}, false};
     std::vector<int64_t> need;
     int64_t b = b0;
     for (; b < batch && b - b0 < p->pq_group; ++b) {
@@ -844,6 +867,7 @@ dc_status dc_doppler_pq(dc_plan_t p, const void *x, void *y, int64_t batch, cons
       }
     }
     g.nb = b - b0;
+    g.identity = need.empty();
     const uint64_t stamp = ++p->pq_clock;
     for (int64_t M : need) {  // hits first, so that misses never evict a table this group uses
       for (int t = 0; t < p->pq_cap; ++t)
@@ -885,6 +909,12 @@ dc_status dc_doppler_pq(dc_plan_t p, const void *x, void *y, int64_t batch, cons
   auto pipeline = [&]() -> dc_status {
     dc_status st = DC_OK;
     for (const Group &g : groups) {
+      if (g.identity) {  // every pulse has M == n: nothing added or removed, y = x ("no work was done")
+        DC_CUDA(cudaMemcpyAsync(yp + g.b0 * n, xp + g.b0 * n, (size_t)(g.nb * n) * sizeof(float2),
+                                cudaMemcpyDeviceToDevice, ln.st),
+                "cudaMemcpyAsync(P/Q identity)");
+        continue;
+      }
       const int64_t l0 = p->pq->launches;
       ProfScope ps(p, DC_K_PQ, g.nb * n, ln.st);
       for (const auto &bm : g.builds) {  // T_M = conj(DFT_L(r)), r = conj(b reflected): FFT(a) T_M = FFT(a) FFT(b)
@@ -939,8 +969,7 @@ dc_status dc_correct(dc_plan_t p, const void *x, void *y, int64_t batch, const d
   const Lane ln{p->stream, 0};
   for (int64_t b0 = 0; b0 < batch && s == DC_OK; b0 += p->chunk) {
     const int64_t nb = std::min(p->chunk, batch - b0);
-    s = run_iono(p, xp + b0 * p->n, p->scratch, nb, pp, b0, 0, ln);
-    if (s == DC_OK) s = run_doppler(p, p->scratch, yp + b0 * p->n, nb, pp, b0, mb, ln);
+    s = run_correct(p, xp + b0 * p->n, yp + b0 * p->n, nb, pp, b0, mb, ln);
   }
   return release_after(p, slot, s);
 }
@@ -1005,8 +1034,7 @@ dc_status dc_correct_host(dc_plan_t p, const void *x_host, void *y_host, int64_t
       DC_CUDA(cudaEventRecord(p->ev_in[i], p->s_h2d), "record");
       DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[i], 0), "wait");
       if (it >= 2) DC_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[i], 0), "wait");  // hout[i] drained
-      if ((s = run_iono(p, p->hin[i], p->scratch, nb, pp, b0, 0, Lane{p->stream, 0})) != DC_OK) return s;
-      if ((s = run_doppler(p, p->scratch, p->hout[i], nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
+      if ((s = run_correct(p, p->hin[i], p->hout[i], nb, pp, b0, mb, Lane{p->stream, 0})) != DC_OK) return s;
       DC_CUDA(cudaEventRecord(p->ev_comp[i], p->stream), "record");
       DC_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[i], 0), "wait");
       DC_CUDA(cudaMemcpyAsync(yh + b0 * pulse_bytes, p->hout[i], nb * pulse_bytes, cudaMemcpyDeviceToHost, p->s_d2h),

@@ -168,3 +168,18 @@ def test_pq_errors(dc):
     with pytest.raises(dc.DispCorrError) as e:
         big.doppler_pq(xb, torch.empty_like(xb), [1.0])
     assert e.value.name == "DC_ERR_INVALID_VALUE"
+
+
+def test_pq_all_identity_batch_is_a_copy(dc):
+    # |n alpha - n| < 1 for every pulse: M == n, nothing added or removed ("no work was done")
+    n = 1 << 16
+    x = synth.complex_gaussian(n, seed=41, batch=5).astype(np.complex64)
+    alphas = [1.0, 1 + 0.4 / n, 1 - 0.9 / n, 1.0, 1 + 0.99 / n]
+    assert all(O.pq_length(n, a) == n for a in alphas)
+    p = dc.Plan(n, 2.048e9, 0.0, taps=8)
+    xd = to_dev(x)
+    yd = to_dev(np.zeros_like(x))
+    l0 = p.info()["kernel_launches"]
+    p.doppler_pq(xd, yd, alphas)
+    assert np.array_equal(from_dev(yd), x)
+    assert p.info()["kernel_launches"] == l0  # a device copy, no kernels

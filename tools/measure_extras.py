@@ -8,6 +8,7 @@
   iono        iono-only throughput at C2 (256 x 2^16) and C3 (64 x 2^20), and the labelled library
               comparator torch.fft.fft -> phase multiply -> torch.fft.ifft (cuFFT, three HBM round trips;
               measurement only, never linked into libdispcorr) on the same inputs
+  pq          E4: FFT P/Q resampling latency per trial at N = 2^19, v ~ U(0, 5 km/s), and batched throughput
 
     python tools/measure_extras.py [latency|sweep|iono|all] [--out profiles/r1_extras.json]
 """
@@ -232,6 +233,56 @@ def c5_accuracy():
     return {"c5_accuracy_vs_analytic": rows, "velocity_mps": 5000.0}
 
 
+def pq_e4():
+    """E4 (fig:pqbenchmark): FFT P/Q resampling of an N = 2^19 pulse (f0 = 420 MHz, B = 18 MHz,
+    T = 500 us -- at fs = 1.048576 GHz the 500 us pulse fits the 2^19 window) with the target
+    velocity drawn from U(0, 5 km/s) per trial: single-pulse latency histogram through dc_doppler_pq
+    (the paper's trial structure), grouped by the number of samples added (M - n), plus batched
+    throughput over the same velocity distribution.  The paper's H100 cluster rates: ~6.5 TS/s (no
+    samples added), 670 MS/s (2 removed), 260 MS/s (4 removed)."""
+    n, fs = 1 << 19, 1.048576e9
+    x0 = synth.lfm(n, fs, 420e6, 18e6, 500e-6, offset=4096).astype(np.complex64)
+    x = torch.from_numpy(np.ascontiguousarray(x0[None])).cuda()
+    y = torch.empty_like(x)
+    st = torch.cuda.current_stream()
+    p = dc.Plan(n, fs, 0.0, taps=8, stream=st)
+    rng = np.random.default_rng(4952)
+    vs = rng.uniform(0.0, 5000.0, 2000)
+    alphas = [dc.alpha_from_velocity(v) for v in vs]
+    # warm every table once (the plan caches one chirp-z table per P/Q length M)
+    for a in sorted(set(alphas), key=lambda a: round((n * a - n) / 2)):
+        p.doppler_pq(x, y, [a])
+    torch.cuda.synchronize()
+    groups = {}
+    evs = []
+    for a in alphas:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        p.doppler_pq(x, y, [a])
+        e1.record(st)
+        evs.append((a, e0, e1))
+    torch.cuda.synchronize()
+    for a, e0, e1 in evs:
+        d = int(2 * round(0.5 * (n * a - n)))
+        groups.setdefault(d, []).append(e0.elapsed_time(e1))
+    out = {"n": n, "fs_hz": fs, "trials": len(alphas), "v_distribution": "U(0, 5 km/s)", "per_added_samples": {}}
+    for d, ts in sorted(groups.items()):
+        st_ = stats_us(ts)
+        st_["samples_per_s_at_p50"] = n / (st_["p50_us"] * 1e-6)
+        st_.pop("hist", None)
+        out["per_added_samples"][str(d)] = st_
+    # batched: 64 pulses per call with velocities from the same distribution
+    batch = 64
+    xb = x.repeat(batch, 1).contiguous()
+    yb = torch.empty_like(xb)
+    ab = [dc.alpha_from_velocity(v) for v in rng.uniform(0.0, 5000.0, batch)]
+    ms = time_calls(lambda: p.doppler_pq(xb, yb, ab), st, 20, warm=3)
+    out["batched"] = {"pulses": batch, "median_ms": float(np.median(ms)),
+                      "samples_per_s": batch * n / (float(np.median(ms)) * 1e-3)}
+    p.close()
+    return out
+
+
 def cpu_oracle():
     """SURVEY 8(d) CPU oracle timing on this box: dc_correct of C4 pulses (2^20, W = 32) in FP64,
     (i) one thread -- the plain definition -- and (ii) all host cores (OpenMP over pulses)."""
@@ -254,7 +305,7 @@ def cpu_oracle():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("what", nargs="?", default="all",
-                    choices=["latency", "sweep", "iono", "iono_sweep", "cpu", "c5acc", "all"])
+                    choices=["latency", "sweep", "iono", "iono_sweep", "cpu", "c5acc", "pq", "all"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0)}
@@ -270,6 +321,8 @@ def main():
         res["cpu_oracle"] = cpu_oracle()
     if a.what in ("c5acc", "all"):
         res["c5_accuracy"] = c5_accuracy()
+    if a.what in ("pq", "all"):
+        res["pq_e4"] = pq_e4()
     s = json.dumps(res, indent=1)
     if a.out:
         open(a.out, "w").write(s + "\n")
