@@ -41,11 +41,11 @@ class DispCorrError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
-KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler", "pq")
+KERNEL_CLASSES = ("iono_small", "fourstep_A", "fourstep_B", "fourstep_C", "doppler", "pq", "correct_fused")
 
 
 class Profile(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6), ("samples", ctypes.c_int64 * 6)]
+    _fields_ = [("launches", ctypes.c_int64 * 7), ("ms", ctypes.c_double * 7), ("samples", ctypes.c_int64 * 7)]
 
 
 class PlanInfo(ctypes.Structure):

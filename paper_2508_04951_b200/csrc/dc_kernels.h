@@ -44,6 +44,10 @@ struct IonoSmallArgs {
 // var: 0 Eq. 15 correction, 1 Eq. 14 distortion, 2 correction + matched filter (T table `ref`),
 // 3 forward spectra stored conjugated to `ref_out` (no inverse transform)
 cudaError_t launch_iono_small(const IonoSmallArgs &a, int var);
+// fused single-round-trip dc_correct (iono + first/second-order Doppler in one kernel, NEXT-1) for
+// single-CTA pulses: n = 2^11 .. 2^13 and W in {16, 32} (correct_small_supported)
+bool correct_small_supported(int log2n, int W);
+cudaError_t launch_correct_small(const IonoSmallArgs &a, float2 *y, double carrier, int W, bool second);
 
 struct FourStepArgs {
   const float2 *src;  // pass A input (pulse-major, pulse_stride apart)

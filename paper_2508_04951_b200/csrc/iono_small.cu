@@ -93,6 +93,58 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   }
 }
 
+// ---- fused single-round-trip dc_correct for single-CTA pulses (NEXT-1): n = 2^11 .. 2^13, W in {16, 32}
+template <int P, int W, bool SECOND>
+static cudaError_t launch_correct_small_pw(const TileArgs &a, cudaStream_t st, int cap) {
+  constexpr int NB = small_nb(P);
+  constexpr int LOGE = small_loge<P>();
+  using CFG = TileCfg<P, LOGE, NB, true, MODE_SMALL>;
+  auto kern = tile_fft_kernel<P, LOGE, NB, true, MODE_SMALL, VAR_CORRECT, W, SECOND>;
+  const size_t smem = CFG::smem_bytes(0, P, true);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CFG::T, smem);
+  const int64_t total = (a.pulses + NB - 1) / NB;
+  int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(CFG::T), smem, st, a);
+}
+template <int P>
+static cudaError_t launch_correct_small_p(const TileArgs &a, int W, bool second, cudaStream_t st, int cap) {
+  if (W == 16) return second ? launch_correct_small_pw<P, 16, true>(a, st, cap) : launch_correct_small_pw<P, 16, false>(a, st, cap);
+  if (W == 32) return second ? launch_correct_small_pw<P, 32, true>(a, st, cap) : launch_correct_small_pw<P, 32, false>(a, st, cap);
+  return cudaErrorInvalidValue;
+}
+
+bool correct_small_supported(int log2n, int W) { return log2n >= 11 && log2n <= 13 && (W == 16 || W == 32); }
+
+cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carrier, int W, bool second) {
+  TileArgs a{};
+  a.src = s.xin;
+  a.dst = nullptr;
+  a.pulses = s.batch;
+  a.pulse_stride = (int64_t)1 << s.log2n;
+  a.pulse_base = 0;
+  a.log2n = s.log2n;
+  a.pp = s.pp;
+  a.twf = s.twf;
+  a.twi = s.twi;
+  a.H = 0;
+  a.fs_over_n = s.fs_over_n;
+  a.fc = s.fc;
+  a.dop_y = y;
+  a.dop_carrier = carrier;
+  switch (s.log2n) {
+    case 11: return launch_correct_small_p<11>(a, W, second, s.stream, s.grid_cap);
+    case 12: return launch_correct_small_p<12>(a, W, second, s.stream, s.grid_cap);
+    case 13: return launch_correct_small_p<13>(a, W, second, s.stream, s.grid_cap);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // Pass plans (radix sequences) exported to the host so it can build the twiddle tables.
 template <int P, int LOGR>
 static void fill_plan(PlanDesc &d) {

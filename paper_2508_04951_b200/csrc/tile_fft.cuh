@@ -12,6 +12,7 @@
 // exchanges between passes use a separate padded work buffer, the last pass stores straight
 // from registers to global memory.
 #pragma once
+#include "doppler_tile.cuh"
 #include "fft_engine.cuh"
 
 namespace dc {
@@ -57,7 +58,16 @@ struct TileArgs {
   const float2 *ref;    // VAR_COMPRESS: T tables (row layout), n entries each
   const int *ref_idx;   // VAR_COMPRESS: per-pulse table index (indexed like pp), or null = table 0
   float2 *ref_out;      // VAR_REFERENCE: conj(X) per pulse (row layout), n entries each
+  float2 *dop_y;        // fused dc_correct (DOPW > 0): Doppler output y[pulses][n]
+  double dop_carrier;   // fused dc_correct: fc / fs (reading R10)
 };
+
+// Fused single-round-trip dc_correct for single-CTA pulses (NEXT-1; DOPW = compile-time Doppler W > 0):
+// the Eq. 15 result of the tile's pulses lands in a zero-margined shared-memory buffer that aliases the
+// work buffer, and the Doppler tile code (doppler_tile.cuh) resamples it straight from there -- x is
+// read and y written once, 16 B/sample for both stages.  Margins of kCsPad zeros on each side hold the
+// window's reach outside [0, n) (R12): W/2 + 1 below, W/2 + R + (n - 1)|beta - 1| above (W <= 64).
+constexpr int kCsPad = 64;
 
 // Shared-memory layout (float2 units): [staging ELEMS][work SMEM_ELEMS][twf][twi][twh][twl]
 template <int P, int LOGE, int NB, bool ROW, int MODE>
@@ -78,13 +88,18 @@ struct TileCfg {
   static __host__ __device__ constexpr int outer_elems(int H, int log2n) {
     return (MODE == MODE_COLA || MODE == MODE_ROWB) ? ((1 << H) + (1 << (log2n - H))) : 0;
   }
-  static __host__ __device__ constexpr size_t smem_bytes(int H, int log2n) {
-    return sizeof(float2) * ((size_t)TL::ELEMS + TL::SMEM_ELEMS + TWF_PAD + TWI_PAD + outer_elems(H, log2n));
+  static __host__ __device__ constexpr size_t smem_bytes(int H, int log2n, bool fused = false) {
+    return sizeof(float2) * ((size_t)TL::ELEMS + TL::SMEM_ELEMS + TWF_PAD + TWI_PAD + outer_elems(H, log2n) +
+                             (fused ? (size_t)(T / 32) * kDopSeg : 0));
   }
+  static constexpr int DSTRIDE = L + 2 * kCsPad;  // fused dc_correct: one zero-margined pulse
 };
 
-template <int P, int LOGE, int NB, bool ROW, int MODE, int VAR>
+template <int P, int LOGE, int NB, bool ROW, int MODE, int VAR, int DOPW = 0, bool DSECOND = false>
 __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_fft_kernel(const TileArgs a) {
+  static_assert(DOPW == 0 || (MODE == MODE_SMALL && VAR == VAR_CORRECT && DOPW <= 64), "fused dc_correct");
+  static_assert(DOPW == 0 || NB * TileCfg<P, LOGE, NB, ROW, MODE>::DSTRIDE <= TileCfg<P, LOGE, NB, ROW, MODE>::TL::SMEM_ELEMS,
+                "the Doppler buffer aliases the work buffer");
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
   using TL = typename CFG::TL;
@@ -105,6 +120,8 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
   float2 *Th = Ti + CFG::TWI_PAD;
   const int H = a.H;
   float2 *Tl = Th + ((MODE == MODE_COLA || MODE == MODE_ROWB) ? (1 << (a.log2n - H)) : 0);
+  float2 *Ob = Tl + ((MODE == MODE_COLA || MODE == MODE_ROWB) ? (1 << H) : 0);  // fused: output staging
+  float2 *D = Wk;  // fused: zero-margined iono result, NB x DSTRIDE (aliases the work buffer)
   const int tid = threadIdx.x;
 
   // ---- geometry of the tile stream
@@ -257,8 +274,9 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
 
     if constexpr (INVP) run_passes<TL, PP, 0, NP - 1, true>(v, Wk, tid, CFG::SMEM_TW ? Ti : a.twi);
 
-    // ---- last pass outputs straight to global memory
+    // ---- last pass outputs straight to global memory (fused dc_correct: to the Doppler buffer)
     constexpr int RO = 1 << (INVP ? PP::log_radix_inv(NP - 1) : PP::log_radix_fwd(NP - 1));
+    if constexpr (DOPW > 0) __syncthreads();  // every thread has loaded its last-pass inputs from Wk = D
 #pragma unroll
     for (int q = 0; q < E / RO; ++q) {
       int b, j;
@@ -267,7 +285,9 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
       for (int r = 0; r < RO; ++r) {
         const int i = j + r * (L / RO);  // output index within FFT b
         float2 val = v[q * RO + r];
-        if constexpr (MODE == MODE_SMALL) {
+        if constexpr (MODE == MODE_SMALL && DOPW > 0) {
+          D[b * CFG::DSTRIDE + kCsPad + i] = val;
+        } else if constexpr (MODE == MODE_SMALL) {
           const int64_t p = pulse + b;
           if (p < a.pulses) __stcs(a.dst + p * L + i, val);
         } else if constexpr (MODE == MODE_ROWB) {
@@ -285,8 +305,37 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
         }
       }
     }
+    if constexpr (DOPW > 0) {
+      // ---- Doppler (Eq. 16 windowed, D1-D4) of the tile's pulses straight from shared memory
+      for (int e = tid; e < NB * 2 * kCsPad; e += T) {
+        const int b = e / (2 * kCsPad), j = e - b * 2 * kCsPad;
+        D[b * CFG::DSTRIDE + (j < kCsPad ? j : L + j)] = make_float2(0.f, 0.f);
+      }
+      __syncthreads();
+      float2 *obw = Ob + (tid >> 5) * kDopSeg;
+      for (int b = 0; b < NB; ++b) {
+        const int64_t p = pulse + b;
+        if (p >= a.pulses) break;
+        DopTile cur;
+        cur.pulse = p;
+        cur.Bcta = -kCsPad;
+        cur.beta = a.pp[a.pulse_base + p].beta;
+        cur.span = 0;
+        cur.pad0 = 0;
+        cur.pad1 = 0;
+        for (int m0 = 0; m0 < L; m0 += T * kDopR) {
+          cur.m0 = m0;
+          if (m0 + (tid >> 5) * kDopSeg < L)  // warps wholly past the pulse end skip
+            dop_tile_compute<DSECOND, DOPW, 0>(D + b * CFG::DSTRIDE, cur, DOPW, obw, a.dop_y, L, a.dop_carrier);
+        }
+      }
+      __syncthreads();  // D is the next item's exchange buffer
+    }
   }
   cp_async_wait_all();
+  if constexpr (DOPW > 0) {
+    if ((tid & 31) == 0) bulk_store_wait_all();  // the warp's last output segment has left shared memory
+  }
 }
 
 }  // namespace dc

@@ -564,3 +564,52 @@ def test_correct_c3_physics_dilated_dispersed_echo(dc):
     iono_only = L.matched_filter_loss_db(from_dev(p.iono(xd.clone(), [tec]))[0], ref)
     # FP64 oracle on the same input: 1.0e-4 dB corrected, 0.093 dB iono-only, 2.15 dB uncorrected
     assert loss < 1e-3 and iono_only > 0.05 and unc > 2.0, (loss, iono_only, unc)
+
+
+# ----------------------------------------------------------------------------- fused single-round-trip dc_correct (NEXT-1)
+@pytest.mark.parametrize("log2n", [11, 12, 13])
+@pytest.mark.parametrize("W", [16, 32])
+@pytest.mark.parametrize("case", ["fast1", "second"])
+def test_correct_fused_small_vs_oracle(dc, log2n, W, case):
+    # n = 2^11 .. 2^13 with W = 16 / 32 and a first/second-order alpha run iono + Doppler in ONE kernel
+    # (the ionospheric result stays in shared memory); parity with the oracle's Doppler(iono(x))
+    import torch
+    n = 1 << log2n
+    # drift |1/alpha - 1| (R/2 + 1/2) within the first-order (<= 2e-4) or second-order (<= 2e-3) range
+    alphas = np.array(ALPHA_CASES["fast1"] if case == "fast1" else [1 + 2e-4, 1 - 3e-4, 1 + 1e-4])
+    alphas = np.append(alphas, 1.0)
+    batch = len(alphas) + 2                       # ragged: not a multiple of the tile's pulses
+    alphas = np.resize(alphas, batch)
+    x = synth.complex_gaussian(n, seed=log2n * 7 + W, batch=batch).astype(np.complex64)
+    tec = np.linspace(0.0, 2e18, batch)
+    for fs, fc in ((2.048e9, 0.0), (51.2e6, 422e6)):
+        p = dc.Plan(n, fs, fc, taps=W)
+        p.profile_enable(True)
+        xd = to_dev(x)
+        yd = torch.empty_like(xd)
+        p.correct(xd, yd, tec, alphas)
+        prof = p.profile_read()
+        assert prof["correct_fused"]["launches"] >= 1 and prof["doppler"]["launches"] == 0
+        ref = O.run_batch("correct", x, fs, fc, W, tec, alphas)
+        assert rel_l2(from_dev(yd), ref).max() < TOL, (fs, fc)
+
+
+def test_correct_fused_falls_back_outside_its_range(dc):
+    # taper, W = 25 and the exact-tap alpha range take the two-kernel path (and still match the oracle)
+    import torch
+    n = 4096
+    x = synth.complex_gaussian(n, seed=5, batch=3).astype(np.complex64)
+    tec = [1e18, 0.0, 5e17]
+    for W, kaiser, alphas in ((25, 0.0, [1 + 3e-5, 1.0, 1 - 2e-5]), (32, 8.0, [1 + 3e-5, 1.0, 1 - 2e-5]),
+                              (32, 0.0, [1.05, 0.97, 1.0])):
+        p = dc.Plan(n, 2.048e9, 0.0, taps=W)
+        if kaiser:
+            p.set_taper(kaiser)
+        p.profile_enable(True)
+        xd = to_dev(x)
+        yd = torch.empty_like(xd)
+        p.correct(xd, yd, tec, alphas)
+        prof = p.profile_read()
+        assert prof["correct_fused"]["launches"] == 0 and prof["doppler"]["launches"] >= 1
+        ref = O.run_batch("correct", x, 2.048e9, 0.0, W, tec, alphas, kaiser=kaiser)
+        assert rel_l2(from_dev(yd), ref).max() < TOL, (W, kaiser)

@@ -13,7 +13,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 COMPONENTS = ["iono8", "iono10", "iono12", "iono14", "iono20", "iono22", "iono24", "doppler", "expand", "compress",
-              "pq", "host"]
+              "fused", "pq", "host"]
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])

@@ -62,6 +62,9 @@ if want("compress"):
         p.compress(x, z, [1e17, 2e17])
         p.compress(x, x, [1e17, 2e17])
         p.sync()
+if want("fused"):
+    run_correct(1 << 12, 5, W=32)                                  # fused single-round-trip dc_correct
+    run_correct(1 << 13, 2, W=16, alphas=[1 + 4e-4, 1 - 4e-4], fc=422e6)
 if want("pq"):
     for n in (256, 1 << 14, 1 << 20):                              # tile / four-step regimes of n and 2n
         p = dc.Plan(n, FS, 422e6 if n == 256 else 0.0, taps=8)
