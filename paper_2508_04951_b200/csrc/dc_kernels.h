@@ -108,7 +108,7 @@ struct DopplerArgs {
 constexpr int kDopMaxCtas = 1024;                       // persistent Doppler grid cap
 constexpr size_t kDopDescBytes = (size_t)kDopMaxCtas * 4 * 48;
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1);
-int doppler_path(double max_abs_beta_m1, bool taper = false);
+int doppler_path(double max_abs_beta_m1, bool taper = false, int W = 32);
 
 // FFT P/Q resampling (pq_kernels.cu, reading R18).  Mv: per-pulse length M (device int[pulses]).
 cudaError_t launch_pq_gather(const float2 *Xc, float2 *a, int64_t pulses, int log2n, int P1, const int *Mv,

@@ -431,7 +431,7 @@ dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
 // n = 2^11 .. 2^13, W in {16, 32}, rectangular window, first/second-order Doppler path; NEXT-1), else
 // the ionospheric stage into the group buffer followed by the Doppler stage
 bool correct_fused_ok(const dc_plan_s *p, double max_abs_beta_m1) {
-  const int path = dc::doppler_path(max_abs_beta_m1, p->taper);
+  const int path = dc::doppler_path(max_abs_beta_m1, p->taper, p->taps);
   return p->regime == 0 && !p->taper && path != 0 && dc::correct_small_supported(p->log2n, p->taps);
 }
 dc_status run_correct(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
@@ -440,7 +440,7 @@ dc_status run_correct(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
     dc::IonoSmallArgs a{src, nullptr, pulses, p->log2n, pp + pulse_base, p->tw_small_f, p->tw_small_i,
                         p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab, nullptr, nullptr, nullptr};
     ProfScope ps(p, DC_K_CORRECT_FUSED, pulses * p->n, ln.st);
-    DC_CUDA(dc::launch_correct_small(a, dst, p->fc / p->fs, p->taps, dc::doppler_path(max_abs_beta_m1) == 2),
+    DC_CUDA(dc::launch_correct_small(a, dst, p->fc / p->fs, p->taps, dc::doppler_path(max_abs_beta_m1, false, p->taps) == 2),
             "fused dc_correct kernel launch");
     return DC_OK;
   }

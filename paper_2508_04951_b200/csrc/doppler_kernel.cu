@@ -50,24 +50,25 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
                         int buf_elems, const __grid_constant__ TaperCoef tc, DopTile *__restrict__ gdesc,
                         const __grid_constant__ CUtensorMap dmap) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
+  constexpr int R = dop_r(WT), M = kDopT * R, SEG = 32 * R;
   extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);                     // kDopBufs x buf_elems input spans
-  float2 *ob = xs + kDopBufs * buf_elems;                            // kDopM output staging (per warp)
+  float2 *ob = xs + kDopBufs * buf_elems;                            // M output staging (per warp)
   // geometry of the tile in each buffer: 128-byte slots (TMA destinations are 128-byte aligned)
-  DopTile *tiles = reinterpret_cast<DopTile *>(ob + kDopM);
+  DopTile *tiles = reinterpret_cast<DopTile *>(ob + M);
   auto dslot = [&](int b) { return reinterpret_cast<DopTile *>(reinterpret_cast<char *>(tiles) + 128 * b); };
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(tiles) + 128 * kDopBufs);  // TMA completion
   uint32_t *released = reinterpret_cast<uint32_t *>(full + kDopBufs);  // warps done with each buffer
   const int W = (WT > 0) ? WT : W_rt;
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t tiles_per_pulse = (uint32_t)((n + kDopM - 1) / kDopM);
+  const uint32_t tiles_per_pulse = (uint32_t)((n + M - 1) / M);
   const uint32_t total = (uint32_t)pulses * tiles_per_pulse;
   if (blockIdx.x >= total) return;
   const uint32_t my_tiles = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
   auto produce = [&](uint32_t i) {  // one thread: stage local tile i into buffer i % kDopBufs (free)
     const int b = (int)(i % kDopBufs);
     const uint32_t it = blockIdx.x + i * gridDim.x;
-    const DopTile t = dop_tile(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
+    const DopTile t = dop_tile<R>(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
     const int slot = (int)blockIdx.x * kDopBufs + b;
     dop_stage_tma(xs + b * buf_elems, t, &xmap, &full[b], dslot(b), gdesc + slot, &dmap, slot);
   };
@@ -80,15 +81,15 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
     for (uint32_t i = 0; i < (uint32_t)kDopBufs && i < my_tiles; ++i) produce(i);
   }
   __syncthreads();
-  float2 *obw = ob + (tid >> 5) * kDopSeg;
+  float2 *obw = ob + (tid >> 5) * SEG;
   for (uint32_t i = 0; i < my_tiles; ++i) {
     const int b = (int)(i % kDopBufs);
     mbar_wait(&full[b], (i / kDopBufs) & 1u);
     const DopTile cur = *dslot(b);
     // a pulse's last tile is ragged: warps whose outputs all lie past n skip it (their issue slots go to
     // the other CTA of the SM), so short pulses waste at most one warp segment instead of a tile
-    if (cur.m0 + (int64_t)(tid >> 5) * kDopSeg < n)
-      dop_tile_compute<SECOND, WT, TAPER>(xs + b * buf_elems, cur, W, obw, y, n, carrier, &tc);
+    if (cur.m0 + (int64_t)(tid >> 5) * SEG < n)
+      dop_tile_compute<SECOND, WT, TAPER, R>(xs + b * buf_elems, cur, W, obw, y, n, carrier, &tc);
     __syncwarp();
     if (lane == 0) {
       // this warp's reads of buffer b are done (release); the last warp out acquires and restages it.
@@ -157,11 +158,12 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
 
 template <bool SECOND, int WT, int TAPER = 0>
 static cudaError_t launch_pipe(const DopplerArgs &a) {
-  const int64_t tiles = (a.n + kDopM - 1) / kDopM * a.pulses;
+  constexpr int R = dop_r(WT), M = kDopT * R;
+  const int64_t tiles = (a.n + M - 1) / M * a.pulses;
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
-  const int span = (int)(kDopM * (1.0 + kDopMaxDrift)) + a.taps + kDopR + 16;
+  const int span = (int)(M * (1.0 + kDopMaxDrift)) + a.taps + R + 16;
   const int buf = (span + kDopBox - 1) / kDopBox * kDopBox;  // whole TMA boxes
-  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + kDopM) + kDopBufs * (128 + sizeof(uint64_t) + 4) + 1024;
+  const size_t smem = sizeof(float2) * (kDopBufs * (size_t)buf + M) + kDopBufs * (128 + sizeof(uint64_t) + 4) + 1024;
   CUtensorMap xmap;
   {
     const uint64_t dims[2] = {(uint64_t)a.n, (uint64_t)a.pulses};
@@ -230,15 +232,16 @@ static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
 //   exact taps otherwise.
 // The tapered weights have the first-order path only (h'' of sinc K is not formed): second-order
 // drifts take the exact path.
-int doppler_path(double max_abs_beta_m1, bool taper) {
-  const double drift = max_abs_beta_m1 * (kDopR / 2 + 0.5);
+int doppler_path(double max_abs_beta_m1, bool taper, int W) {
+  const int R = (W == 128) ? dop_r(128) : kDopR;  // the fast kernel's R for this W (compile-time W only)
+  const double drift = max_abs_beta_m1 * (R / 2 + 0.5);
   if (drift <= 2.0e-4) return 1;
   if (drift <= kDopMaxDrift && !taper) return 2;
   return 0;
 }
 
 cudaError_t launch_doppler(const DopplerArgs &a, double max_abs_beta_m1) {
-  const int path = doppler_path(max_abs_beta_m1, a.taper);
+  const int path = doppler_path(max_abs_beta_m1, a.taper, a.taps);
   if (path == 0) return launch_doppler_exact(a);
   return launch_doppler_fast(a, path == 2);
 }

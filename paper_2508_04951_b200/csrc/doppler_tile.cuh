@@ -14,14 +14,17 @@ constexpr int kDopT = 256;  // threads per CTA (8 consumer warps)
 #define DC_DOP_R 11
 #endif
 constexpr int kDopR = DC_DOP_R;  // outputs per thread: odd, so lanes' windows (R samples apart) hit distinct banks
-constexpr int kDopM = kDopT * kDopR;     // outputs per tile
+// R per compile-time W: R = 9 at W = 128 (the 129-tap loop of R = 11 is register-bound: 58 vs 45 GS/s
+// measured), 11 otherwise (W = 32: 201 vs 190 GS/s for R = 9, 146 for R = 13)
+__host__ __device__ constexpr int dop_r(int WT) { return WT >= 128 ? 9 : kDopR; }
+constexpr int kDopM = kDopT * kDopR;     // outputs per tile (R = kDopR)
 constexpr int kDopSeg = 32 * kDopR;      // outputs per warp (even: 16-byte aligned bulk stores)
 constexpr double kDopMaxDrift = 2.0e-3;  // max |beta - 1| * R / 2 for the fast path
 #ifndef DC_DOP_NBUF
 #define DC_DOP_NBUF 3
 #endif
 constexpr int kDopBufs = DC_DOP_NBUF;    // input staging buffers (tile i + kDopBufs is staged once tile i is read)
-static_assert(kDopSeg % 2 == 0, "warp segments must be 16-byte multiples");
+static_assert(kDopSeg % 2 == 0 && (32 * dop_r(128)) % 2 == 0, "warp segments must be 16-byte multiples");
 
 __device__ __forceinline__ float frcp(float x) {
   float r;
@@ -42,18 +45,20 @@ static_assert(sizeof(DopTile) == 48, "bulk copies move multiples of 16 bytes");
 // tile `item` = (pulse, tile of kDopM outputs) -- 32-bit index arithmetic (items < 2^32: pulses per
 // launch <= 65535, tiles per pulse <= 2^24 / kDopM); beta = that pulse's 1/alpha
 __device__ __forceinline__ uint32_t dop_pulse(uint32_t item, uint32_t tiles_per_pulse) { return item / tiles_per_pulse; }
+template <int R = kDopR>
 __device__ __forceinline__ DopTile dop_tile(uint32_t item, uint32_t tiles_per_pulse, int W, double beta) {
+  constexpr int M = kDopT * R;
   DopTile t;
   const uint32_t pulse = item / tiles_per_pulse;
   t.pulse = pulse;
-  t.m0 = (int64_t)(item - pulse * tiles_per_pulse) * kDopM;
+  t.m0 = (int64_t)(item - pulse * tiles_per_pulse) * M;
   t.beta = beta;
   const double halfW = 0.5 * (double)W;
   const int lo_shift = (t.beta < 1.0) ? 1 : 0;
   t.Bcta = (int64_t)floor((double)t.m0 * t.beta - halfW) + 1 - lo_shift;
   t.Bcta -= (t.Bcta & 1);  // TMA boxes must start 16-byte aligned: even sample index
-  const int64_t mlast = t.m0 + kDopM - 1;
-  const int64_t Kend = (int64_t)floor((double)mlast * t.beta - halfW) + 1 + W + kDopR + 4;
+  const int64_t mlast = t.m0 + M - 1;
+  const int64_t Kend = (int64_t)floor((double)mlast * t.beta - halfW) + 1 + W + R + 4;
   t.span = (int)(Kend - t.Bcta);
   t.pad0 = 0;
   t.pad1 = 0;
@@ -122,16 +127,17 @@ __device__ __forceinline__ void taper_eval(const TaperCoef &tc, float d, float &
 // rounding, so when the first and last outputs are on the same side by a clear margin all R decisions
 // agree; only a thread whose outputs straddle a window step (~R |beta - 1| of all threads) evaluates
 // each output.  Returns the bit set {r : a_r = 1}.
+template <int R = kDopR>
 __device__ __forceinline__ uint32_t dop_membership(double md, double beta, double halfW, double Bd, double x0) {
-  constexpr uint32_t kAll = (1u << kDopR) - 1u;
+  constexpr uint32_t kAll = (1u << R) - 1u;
   constexpr double kMargin = 1.0e-7;  // >> rounding of t (ulp(2^25) = 7.5e-9)
   const double X0 = x0 - Bd;          // exact (Sterbenz: |x0 - Bd| <= 1)
-  const double XL = __dsub_rn(__dmul_rn(md + (double)(kDopR - 1), beta), halfW) - (Bd + (double)(kDopR - 1));
+  const double XL = __dsub_rn(__dmul_rn(md + (double)(R - 1), beta), halfW) - (Bd + (double)(R - 1));
   if (X0 >= kMargin && XL >= kMargin) return kAll;
   if (X0 <= -kMargin && XL <= -kMargin) return 0u;
   uint32_t own1 = 0;
 #pragma unroll 1
-  for (int r = 0; r < kDopR; ++r)
+  for (int r = 0; r < R; ++r)
     own1 |= (__dsub_rn(__dmul_rn(md + (double)r, beta), halfW) >= Bd + (double)r) ? (1u << r) : 0u;
   return own1;
 }
@@ -141,32 +147,33 @@ __device__ __forceinline__ uint32_t dop_membership(double md, double beta, doubl
 // (kDopSeg samples) as ONE bulk async copy issued by lane 0 (no LDS/STG per output, no CTA barrier).
 // TAPER > 0: tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only): the Hann window
 // (TAPER == kTaperHann) or a Kaiser window of TAPER series terms.
-template <bool SECOND, int WT, int TAPER = 0>
+template <bool SECOND, int WT, int TAPER = 0, int R = dop_r(WT)>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
                                                  double carrier, const TaperCoef *tcp = nullptr) {
   static_assert(!(TAPER > 0 && SECOND), "the tapered path is first order");
+  constexpr int SEG = 32 * R;  // outputs per warp
   const int W = (WT > 0) ? WT : W_rt;
   const double halfW = 0.5 * (double)W;
   const int tid = threadIdx.x, lane = tid & 31;
   // ---- this thread's R consecutive outputs: exact binary64 window bookkeeping.  Window decisions
   // use the oracle's two separately rounded binary64 operations fl(fl(m beta) - W/2) (__dmul_rn /
   // __dsub_rn: never contracted into an FMA), so membership matches R9 exactly.
-  const int64_t mt = cur.m0 + (int64_t)tid * kDopR;
+  const int64_t mt = cur.m0 + (int64_t)tid * R;
   const double beta = cur.beta;
   const int lo_shift = (beta < 1.0) ? 1 : 0;
   const double md = (double)mt;
   const double x0 = __dsub_rn(__dmul_rn(md, beta), halfW);
   const int64_t B = (int64_t)floor(x0) + 1 - lo_shift;  // union base: x[B + i], i = 0 .. W + R - 1
   const double Bd = (double)B;
-  const uint32_t own1 = dop_membership(md, beta, halfW, Bd, x0);
+  const uint32_t own1 = dop_membership<R>(md, beta, halfW, Bd, x0);
   // Taylor steps delta_r = (r - R/2)(beta - 1): pairs for FFMA2 (+ one single for odd R)
-  constexpr int RC = kDopR / 2;  // reference output
+  constexpr int RC = R / 2;  // reference output
   const float db = (float)(beta - 1.0);
-  float2 dl[kDopR / 2];
+  float2 dl[R / 2];
 #pragma unroll
-  for (int h = 0; h < kDopR / 2; ++h) dl[h] = make_float2((2 * h - RC) * db, (2 * h + 1 - RC) * db);
-  const float dlast = (kDopR - 1 - RC) * db;  // the unpaired last output (odd R)
+  for (int h = 0; h < R / 2; ++h) dl[h] = make_float2((2 * h - RC) * db, (2 * h + 1 - RC) * db);
+  const float dlast = (R - 1 - RC) * db;  // the unpaired last output (odd R)
   // Reference position (output RC) relative to the union's middle tap Mi = floor(W/2): vrel lies in
   // (-1.0002, 1.5002), so the sample nearest to it is union tap Mi + k0, k0 = rint(vrel) in {-1, .., 2}.
   // Union tap jj = Mi + k sits at distance d_k = vrel - k.  Taps k != k0 (|d| >= 1/2) take d = uf - k, one
@@ -180,7 +187,11 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   const float u = __double2float_rn(vrel - k0d);
   const float uf = __double2float_rn(vrel);
   float S, Cc;
+#if DC_DOP_SFU_SINCOS
+  __sincosf(3.14159265358979f * u, &S, &Cc);  // |u| <= 1/2: SFU, absolute error ~4e-7
+#else
   sincospif(u, &S, &Cc);
+#endif
   S *= 0.31830988618379067f;  // sin(pi u) / pi
   float wc, w1c, w2c;
   {
@@ -198,14 +209,14 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   }
   const float2 *xb = sb + (B - cur.Bcta);  // x[B + i] = xb[i]
   const float Sp = (k0 & 1) ? -S : S, Cp = (k0 & 1) ? -Cc : Cc;
-  float2 acc[kDopR];
+  float2 acc[R];
 #pragma unroll
-  for (int r = 0; r < kDopR; ++r) acc[r] = make_float2(0.f, 0.f);
+  for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
   auto mac = [&](const float2 *xv, float w, float w1, float w2, auto EDGEc) {
     constexpr int EDGE = decltype(EDGEc)::value;
     auto keep = [&](int r) { return EDGE == 0 || (((own1 >> r) & 1u) == (EDGE == 2 ? 1u : 0u)); };
 #pragma unroll
-    for (int h = 0; h < kDopR / 2; ++h) {
+    for (int h = 0; h < R / 2; ++h) {
       float2 hh;
       if (SECOND) {
         float2 t = __ffma2_rn(make_float2(0.5f * w2, 0.5f * w2), dl[h], make_float2(w1, w1));
@@ -220,10 +231,10 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       acc[2 * h] = __ffma2_rn(xv[2 * h], make_float2(hh.x, hh.x), acc[2 * h]);
       acc[2 * h + 1] = __ffma2_rn(xv[2 * h + 1], make_float2(hh.y, hh.y), acc[2 * h + 1]);
     }
-    if constexpr (kDopR & 1) {
+    if constexpr (R & 1) {
       float hl = SECOND ? fmaf(fmaf(0.5f * w2, dlast, w1), dlast, w) : fmaf(w1, dlast, w);
-      if (EDGE) hl = keep(kDopR - 1) ? hl : 0.f;
-      acc[kDopR - 1] = __ffma2_rn(xv[kDopR - 1], make_float2(hl, hl), acc[kDopR - 1]);
+      if (EDGE) hl = keep(R - 1) ? hl : 0.f;
+      acc[R - 1] = __ffma2_rn(xv[R - 1], make_float2(hl, hl), acc[R - 1]);
     }
   };
   // weights of union tap jj = Mi + k at distance d: sinc = (-1)^k Sp / d, sinc' = ((-1)^k Cp - sinc) / d,
@@ -251,9 +262,9 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   // distance of union tap Mi + k
   auto dist = [&](int k) { return ((WT == 0 || (k >= -1 && k <= 2)) && k == k0) ? u : uf - (float)k; };
   {
-    float2 xw[kDopR];
+    float2 xw[R];
 #pragma unroll
-    for (int r = 0; r < kDopR; ++r) xw[r] = xb[r];
+    for (int r = 0; r < R; ++r) xw[r] = xb[r];
     {
       float w, w1, w2;
       weights(-Mi, dist(-Mi), w, w1, w2);
@@ -261,8 +272,8 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
     }
     auto step = [&](int jj) {
 #pragma unroll
-      for (int r = 0; r < kDopR - 1; ++r) xw[r] = xw[r + 1];
-      xw[kDopR - 1] = xb[jj + kDopR - 1];
+      for (int r = 0; r < R - 1; ++r) xw[r] = xw[r + 1];
+      xw[R - 1] = xb[jj + R - 1];
       float w, w1, w2;
       weights(jj - Mi, dist(jj - Mi), w, w1, w2);
       mac(xw, w, w1, w2, std::integral_constant<int, 0>());
@@ -276,8 +287,8 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
     }
     {
 #pragma unroll
-      for (int r = 0; r < kDopR - 1; ++r) xw[r] = xw[r + 1];
-      xw[kDopR - 1] = xb[W + kDopR - 1];
+      for (int r = 0; r < R - 1; ++r) xw[r] = xw[r + 1];
+      xw[R - 1] = xb[W + R - 1];
       float w, w1, w2;
       weights(W - Mi, dist(W - Mi), w, w1, w2);
       mac(xw, w, w1, w2, std::integral_constant<int, 2>());
@@ -288,7 +299,7 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   const double g = carrier * (1.0 - beta);
   if (g != 0.0) {
 #pragma unroll
-    for (int r = 0; r < kDopR; ++r) {
+    for (int r = 0; r < R; ++r) {
       const double psi = g * (double)(mt + r);
       acc[r] = cmul(acc[r], expm2pi(__double2float_rn(psi - rint(psi))));
     }
@@ -298,12 +309,12 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   if (lane == 0) bulk_store_wait_read();
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < kDopR; ++r) ob[lane * kDopR + r] = acc[r];
+  for (int r = 0; r < R; ++r) ob[lane * R + r] = acc[r];
   fence_proxy_async();  // generic-proxy writes -> visible to the bulk copy (async proxy)
   __syncwarp();
   if (lane == 0) {
-    const int64_t mw = cur.m0 + (int64_t)(tid >> 5) * kDopSeg;
-    const int64_t valid = min((int64_t)kDopSeg, n - mw);  // even: n and mw are even
+    const int64_t mw = cur.m0 + (int64_t)(tid >> 5) * SEG;
+    const int64_t valid = min((int64_t)SEG, n - mw);  // even: n and mw are even
     if (valid > 0) {
       bulk_store(y + cur.pulse * n + mw, ob, (unsigned)(valid * sizeof(float2)));
       bulk_commit();
