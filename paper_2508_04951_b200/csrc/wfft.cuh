@@ -218,7 +218,6 @@ __global__ void __launch_bounds__(NW * 32, 1) warp_row_kernel(const WarpArgs a) 
 #pragma unroll
           for (int s = 0; s < 32; ++s) rc[s] = __ldg(rtab + lane + 32 * s);
         }
-#pragma unroll
         uint32_t ex = 0u;  // elements needing the exact binary64 phase (phase_exact_fixup)
 #pragma unroll
         for (int s = 0; s < 32; ++s) {
