@@ -40,17 +40,15 @@ namespace dc {
 // reaches the consumers through the TMA engine too (from a per-CTA global slot), counted by the same
 // `full` barrier as the data.
 // WT > 0: the tap count W is a compile-time constant (fully unrolled tap loop); WT = 0: runtime W.
-#ifndef DC_DOP_MINB
-#define DC_DOP_MINB 2
-#endif
-template <bool SECOND, int WT, int TAPER>
-__global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
+// T threads per CTA at 128 registers: 2 CTAs per SM for T = 256, 1 for T = 512, 4 for T = 128
+template <bool SECOND, int WT, int TAPER, int T>
+__global__ void __launch_bounds__(T, 65536 / (T * 128))
     doppler_pipe_kernel(const __grid_constant__ CUtensorMap xmap, float2 *__restrict__ y, int64_t n, int W_rt,
                         const PulseParams *__restrict__ pp, int64_t pulse_base, double carrier, int64_t pulses,
                         int buf_elems, const __grid_constant__ TaperCoef tc, DopTile *__restrict__ gdesc,
                         const __grid_constant__ CUtensorMap dmap) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
-  constexpr int R = dop_r(WT), M = kDopT * R, SEG = 32 * R;
+  constexpr int R = dop_r(WT), M = T * R, SEG = 32 * R;
   extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);                     // kDopBufs x buf_elems input spans
   float2 *ob = xs + kDopBufs * buf_elems;                            // M output staging (per warp)
@@ -68,7 +66,7 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
   auto produce = [&](uint32_t i) {  // one thread: stage local tile i into buffer i % kDopBufs (free)
     const int b = (int)(i % kDopBufs);
     const uint32_t it = blockIdx.x + i * gridDim.x;
-    const DopTile t = dop_tile<R>(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
+    const DopTile t = dop_tile<R, T>(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
     const int slot = (int)blockIdx.x * kDopBufs + b;
     dop_stage_tma(xs + b * buf_elems, t, &xmap, &full[b], dslot(b), gdesc + slot, &dmap, slot);
   };
@@ -95,7 +93,7 @@ __global__ void __launch_bounds__(kDopT, DC_DOP_MINB)
       // this warp's reads of buffer b are done (release); the last warp out acquires and restages it.
       // Nobody else touches released[b] until tile i + kDopBufs -- the one staged here -- is consumed.
       __threadfence_block();
-      if (atomicAdd(&released[b], 1u) == (uint32_t)(kDopT / 32 - 1)) {
+      if (atomicAdd(&released[b], 1u) == (uint32_t)(T / 32 - 1)) {
         released[b] = 0u;
         __threadfence_block();
         if (i + kDopBufs < my_tiles) produce(i + kDopBufs);
@@ -156,9 +154,9 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
   y[pulse * n + m] = acc;
 }
 
-template <bool SECOND, int WT, int TAPER = 0>
+template <bool SECOND, int WT, int TAPER, int T>
 static cudaError_t launch_pipe(const DopplerArgs &a) {
-  constexpr int R = dop_r(WT), M = kDopT * R;
+  constexpr int R = dop_r(WT), M = T * R;
   const int64_t tiles = (a.n + M - 1) / M * a.pulses;
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
   const int span = (int)(M * (1.0 + kDopMaxDrift)) + a.taps + R + 16;
@@ -171,13 +169,13 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
     const uint32_t box[2] = {(uint32_t)kDopBox, 1u};
     if (!encode_tile_map(&xmap, a.x, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
   }
-  auto kern = doppler_pipe_kernel<SECOND, WT, TAPER>;
+  auto kern = doppler_pipe_kernel<SECOND, WT, TAPER, T>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 2;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDopT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
   grid = std::min<int64_t>(grid, kDopMaxCtas);
@@ -189,20 +187,38 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
     const uint32_t box[2] = {6u, 1u};
     if (!encode_tile_map(&dmap, a.desc, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
   }
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(kDopT), smem, a.stream, xmap, a.y, a.n, a.taps, a.pp, a.pulse_base,
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(T), smem, a.stream, xmap, a.y, a.n, a.taps, a.pp, a.pulse_base,
                     a.carrier_cycles_per_sample, a.pulses, buf, a.tc, reinterpret_cast<DopTile *>(a.desc), dmap);
+}
+
+// CTA size per configuration (measured, W = 32 at 2^20 / 4096: T = 256 191.8 / 127.8, T = 512 201.0 / 132.8,
+// T = 128 187.5 / 169.2 GS/s): short pulses (n < 2^16, a few tiles per pulse) take 128-thread CTAs (4 per
+// SM: finer tiles, less quantisation); long pulses 512 (one 16-warp CTA per SM: one set of staging buffers
+// and fewer, longer tiles), except W <= 16 (256: 303 vs 286 GS/s) and the tapered windows (256).
+template <bool SECOND, int WT, int TAPER>
+static cudaError_t launch_pipe_t(const DopplerArgs &a) {
+  if constexpr (TAPER == 0) {
+    if (a.n < (1 << 16)) return launch_pipe<SECOND, WT, TAPER, 128>(a);
+    if constexpr (WT == 0 || WT > 16) {
+      return launch_pipe<SECOND, WT, TAPER, 512>(a);
+    } else {
+      return launch_pipe<SECOND, WT, TAPER, 256>(a);
+    }
+  } else {
+    return launch_pipe<SECOND, WT, TAPER, 256>(a);
+  }
 }
 
 template <bool SECOND, int TAPER = 0>
 static cudaError_t launch_pipe_w(const DopplerArgs &a) {
   switch (a.taps) {  // compile-time tap counts of the benchmark / sweep configurations
-    case 8: return launch_pipe<SECOND, 8, TAPER>(a);
-    case 16: return launch_pipe<SECOND, 16, TAPER>(a);
-    case 25: return launch_pipe<SECOND, 25, TAPER>(a);
-    case 32: return launch_pipe<SECOND, 32, TAPER>(a);
-    case 64: return launch_pipe<SECOND, 64, TAPER>(a);
-    case 128: return launch_pipe<SECOND, 128, TAPER>(a);
-    default: return launch_pipe<SECOND, 0, TAPER>(a);
+    case 8: return launch_pipe_t<SECOND, 8, TAPER>(a);
+    case 16: return launch_pipe_t<SECOND, 16, TAPER>(a);
+    case 25: return launch_pipe_t<SECOND, 25, TAPER>(a);
+    case 32: return launch_pipe_t<SECOND, 32, TAPER>(a);
+    case 64: return launch_pipe_t<SECOND, 64, TAPER>(a);
+    case 128: return launch_pipe_t<SECOND, 128, TAPER>(a);
+    default: return launch_pipe_t<SECOND, 0, TAPER>(a);
   }
 }
 

@@ -9,7 +9,9 @@
 
 namespace dc {
 
-constexpr int kDopT = 256;  // threads per CTA (8 consumer warps)
+// threads per CTA of the Doppler pipeline kernel: a template parameter chosen per launch (doppler_kernel.cu);
+// kDopT is the default (tapered windows, W = 16) and the unit of the tile-geometry constants below
+constexpr int kDopT = 256;
 #ifndef DC_DOP_R
 #define DC_DOP_R 11
 #endif
@@ -45,9 +47,9 @@ static_assert(sizeof(DopTile) == 48, "bulk copies move multiples of 16 bytes");
 // tile `item` = (pulse, tile of kDopM outputs) -- 32-bit index arithmetic (items < 2^32: pulses per
 // launch <= 65535, tiles per pulse <= 2^24 / kDopM); beta = that pulse's 1/alpha
 __device__ __forceinline__ uint32_t dop_pulse(uint32_t item, uint32_t tiles_per_pulse) { return item / tiles_per_pulse; }
-template <int R = kDopR>
+template <int R = kDopR, int T = kDopT>
 __device__ __forceinline__ DopTile dop_tile(uint32_t item, uint32_t tiles_per_pulse, int W, double beta) {
-  constexpr int M = kDopT * R;
+  constexpr int M = T * R;
   DopTile t;
   const uint32_t pulse = item / tiles_per_pulse;
   t.pulse = pulse;
