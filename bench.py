@@ -310,7 +310,7 @@ def main():
     tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
     tfile = tfiles[-1] if tfiles else ""  # the latest round's capture of the kernels as built
     kname = {"fourstep_A": "warp_col3_kernel<0>", "fourstep_B": "warp_row_kernel<2", "fourstep_C": "warp_col3_kernel<1>",
-             "doppler": "doppler_pipe_kernel<0, 32, 0>"}.get(dom)
+             "doppler": "doppler_pipe_kernel<0, 32, 0"}.get(dom)
     if os.path.exists(tfile) and kname and n == (1 << 20):
         per = json.load(open(tfile))["dram_bytes_per_sample"]
         hit = [v for k, v in per.items() if kname in k]
@@ -333,7 +333,7 @@ def main():
                               "ceiling_samples_per_s": ceil, "frac_of_ceiling": fft_stage["samples_per_s"] / ceil,
                               "ceiling": "min(HBM at 16 B/sample, FP32 pipe at the counted lane-ops)",
                               "counters": os.path.relpath(ofiles[-1], ROOT)})
-        per_d = lane_ops("doppler_pipe_kernel<0, 32, 0>")
+        per_d = lane_ops("doppler_pipe_kernel<0, 32, 0")
         if per_d and "doppler" in kern:
             sps = kern["doppler"]["samples_per_launch"] / (kern["doppler"]["ms_per_launch"] / 1e3)
             kern["doppler"].update({"fp32_lane_ops_per_sample": per_d, "fp32_pipe_ceiling_samples_per_s": lanes / per_d,

@@ -7,6 +7,17 @@
 
 namespace dc {
 
+// cached launch preparation (launch_cache.cu): sets the kernel's dynamic shared-memory limit once and
+// returns the SM count and resident CTAs per SM for (kernel, current device, block size, smem)
+struct LaunchShape {
+  int sms, per_sm;
+};
+cudaError_t launch_shape(const void *fn, int threads, size_t smem, LaunchShape *out);
+template <class K>
+inline cudaError_t launch_shape(K *fn, int threads, size_t smem, LaunchShape *out) {
+  return launch_shape(reinterpret_cast<const void *>(fn), threads, smem, out);
+}
+
 constexpr int kMaxPasses = 8;
 
 // radix sequence of one FFT size, as compiled into the kernels (for twiddle-table building)

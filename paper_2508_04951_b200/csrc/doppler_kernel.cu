@@ -170,12 +170,10 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
     if (!encode_tile_map(&xmap, a.x, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
   }
   auto kern = doppler_pipe_kernel<SECOND, WT, TAPER, T>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, T, smem, &ls);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 2;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+  const int sms = ls.sms, per_sm = ls.per_sm;
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
   grid = std::min<int64_t>(grid, kDopMaxCtas);

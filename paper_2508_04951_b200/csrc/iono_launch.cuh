@@ -31,12 +31,10 @@ static cudaError_t launch_tile_cfg(const TileArgs &a, int64_t total, cudaStream_
   using CFG = TileCfg<P, LOGE, NB, ROW, MODE>;
   auto kern = tile_fft_kernel<P, LOGE, NB, ROW, MODE, VAR>;
   const size_t smem = CFG::smem_bytes(a.H, a.log2n);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, CFG::T, smem, &ls);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CFG::T, smem);
+  const int sms = ls.sms, per_sm = ls.per_sm;
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   return launch_pdl(kern, dim3((unsigned)grid), dim3(CFG::T), smem, st, a);
@@ -50,12 +48,10 @@ static size_t warp_row_smem(int log2n, int H, bool outer) {
 template <class K>
 static cudaError_t launch_persistent(K kern, size_t smem, int64_t total, const WarpArgs &a, cudaStream_t st, int cap,
                                      int nw = kWW) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, nw * 32, smem, &ls);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+  const int sms = ls.sms, per_sm = ls.per_sm;
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   return launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, st, a);
@@ -94,12 +90,10 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
   const size_t launch_smem = warp_col3_smem_bytes();
   auto kern = inv ? warp_col3_kernel<true> : warp_col3_kernel<false>;
   constexpr int threads = 2 * kWW * 32;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)launch_smem);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, threads, launch_smem, &ls);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, launch_smem);
+  const int sms = ls.sms, per_sm = ls.per_sm;
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   return launch_pdl(kern, dim3((unsigned)grid), dim3(threads), launch_smem, st, a, smap);
@@ -107,10 +101,10 @@ static cudaError_t launch_warp_col(const WarpArgs &a, bool inv, cudaStream_t st,
 template <int N1>
 static cudaError_t launch_tcol_n(const WarpArgs &a, bool inv, cudaStream_t st, int cap) {
   auto kern = inv ? thread_col_kernel<N1, true> : thread_col_kernel<N1, false>;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcolT, 0);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, kTcolT, 0, &ls);
+  if (e != cudaSuccess) return e;
+  const int sms = ls.sms, per_sm = ls.per_sm;
   const int64_t items = a.pulses * (1024 / 32);  // warp items
   int64_t grid = std::min<int64_t>((items + kTcolT / 32 - 1) / (kTcolT / 32), (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);

@@ -38,11 +38,10 @@ template <int N1>
 static cudaError_t launch_wsmall(const WarpArgs &a, int var, cudaStream_t st, int cap) {
   auto kern = (var == VAR_DISTORT) ? warp_small_kernel<N1, VAR_DISTORT> : warp_small_kernel<N1, VAR_CORRECT>;
   const size_t smem = wsmall_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, kWsT, smem, &ls);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = ls.sms;
   const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
   int64_t grid = std::min<int64_t>(tiles, sms);
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
@@ -101,12 +100,10 @@ static cudaError_t launch_correct_small_pw(const TileArgs &a, cudaStream_t st, i
   using CFG = TileCfg<P, LOGE, NB, true, MODE_SMALL>;
   auto kern = tile_fft_kernel<P, LOGE, NB, true, MODE_SMALL, VAR_CORRECT, W, SECOND>;
   const size_t smem = CFG::smem_bytes(0, P, true);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, CFG::T, smem, &ls);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CFG::T, smem);
+  const int sms = ls.sms, per_sm = ls.per_sm;
   const int64_t total = (a.pulses + NB - 1) / NB;
   int64_t grid = std::min<int64_t>(total, (int64_t)sms * std::max(per_sm, 1));
   if (cap > 0) grid = std::min<int64_t>(grid, cap);

@@ -119,11 +119,10 @@ __global__ void __launch_bounds__(256) pq_post_kernel(const float2 *__restrict__
 }
 
 static int ew_grid(int64_t total) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  LaunchShape ls{148, 8};
+  launch_shape(pq_post_kernel, 256, 0, &ls);  // (cached) SM count of the current device
   const int64_t want = (total + 255) / 256;
-  return (int)std::min<int64_t>(want, (int64_t)sms * 8);
+  return (int)std::min<int64_t>(want, (int64_t)ls.sms * 8);
 }
 
 cudaError_t launch_pq_gather(const float2 *Xc, float2 *a, int64_t pulses, int log2n, int P1, const int *Mv,
