@@ -607,17 +607,20 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
   p->chunk = std::max<int64_t>(1, kChunkTargetBytes / (n * (int64_t)sizeof(float2)));
   // per-bin g_k = 1/f_k (0 where f_k <= 0, reading R3) for the warp-level row kernel, FP32 pairs:
   // regime 0 (n = 1024): natural bin order; four-step with N2 = 1024: row layout [k1][k2] of k = k1 + N1 k2
-  if (p->tw1024) {
-    const int P1 = (p->regime == 0 && p->log2n == 10) ? 0 : p->P1;
+  // regime 0, n = 128 .. 1024 (the warp-level kernels): natural bin order
+  const bool tiny = p->regime == 0 && p->log2n >= 7 && p->log2n <= 10;
+  if (p->tw1024 || tiny) {
+    const int P1 = tiny ? 0 : p->P1;
+    const int64_t N2 = tiny ? n : 1024;
     std::vector<float2> g((size_t)n);
     for (int64_t k1 = 0; k1 < (1ll << P1); ++k1)
-      for (int64_t k2 = 0; k2 < 1024; ++k2) {
+      for (int64_t k2 = 0; k2 < N2; ++k2) {
         const int64_t k = k1 + (k2 << P1);
         const int64_t kk = (k >= n / 2) ? k - n : k;
         const double f = fc_hz + fs_hz * (double)kk / (double)n;
         const double gi = (f > 0.0) ? 1.0 / f : 0.0;
         const float hi = (float)gi;
-        g[(size_t)(k1 * 1024 + k2)] = make_float2(hi, (float)(gi - (double)hi));
+        g[(size_t)(k1 * N2 + k2)] = make_float2(hi, (float)(gi - (double)hi));
       }
     if ((s = upload(&p->gtab, g)) != DC_OK) return cleanup(s);
   }

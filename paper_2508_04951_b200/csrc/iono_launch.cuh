@@ -6,6 +6,7 @@
 #include "wfft.cuh"
 #include "tcol.cuh"
 #include "wsmall.cuh"
+#include "wtiny.cuh"
 #include "tma_host.h"
 
 #include <algorithm>

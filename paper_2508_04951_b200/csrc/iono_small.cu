@@ -48,6 +48,19 @@ static cudaError_t launch_wsmall(const WarpArgs &a, int var, cudaStream_t st, in
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kWsT), smem, st, a);
 }
 
+template <int Q>
+static cudaError_t launch_wtiny(const WarpArgs &a, int var, cudaStream_t st, int cap) {
+  auto kern = (var == VAR_DISTORT) ? warp_tiny_kernel<Q, VAR_DISTORT> : warp_tiny_kernel<Q, VAR_CORRECT>;
+  const size_t smem = wtiny_smem_bytes(32 * Q);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, kTinyNW * 32, smem, &ls);
+  if (e != cudaSuccess) return e;
+  const int64_t items = (a.pulses + (32 / Q) - 1) / (32 / Q);
+  int64_t grid = std::min<int64_t>((items + kTinyNW - 1) / kTinyNW, (int64_t)ls.sms * ls.per_sm);
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kTinyNW * 32), smem, st, a);
+}
+
 cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   TileArgs a{};
   a.src = s.xin;
@@ -67,6 +80,13 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   a.ref_out = s.ref_out;
   if (s.log2n == 10 && s.tw1024 && s.gtab)
     return launch_warp_row<MODE_SMALL>(warp_args(a, s.tw1024, s.gtab), var, s.stream, s.grid_cap);
+  // n = 128 .. 512: warp-level kernel (wtiny.cuh) for the correction / forward model
+  if (s.log2n >= 7 && s.log2n <= 9 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
+    const WarpArgs w = warp_args(a, nullptr, s.gtab);
+    if (s.log2n == 7) return launch_wtiny<4>(w, var, s.stream, s.grid_cap);
+    if (s.log2n == 8) return launch_wtiny<8>(w, var, s.stream, s.grid_cap);
+    return launch_wtiny<16>(w, var, s.stream, s.grid_cap);
+  }
   // in-CTA four-step on the warp FFT (wsmall.cuh) for 4096 / 8192: +5 % / +18 % over the tile
   // kernel; for 2048 the tile kernel is faster (128 vs 148 GS/s measured) and stays.  Pulse
   // compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).

@@ -55,10 +55,10 @@ __device__ __forceinline__ float2 twn(uint32_t m, int log2n) {
 // samples go through its exchange buffer (each lane touches only its own slots) so that the
 // out-of-line binary64 routine is called from a loop with no sample registers live -- 32 inline
 // call sites in the phase loop cost the row pass 2.4x (measured, round 2).
-template <bool DISTORT, class KB>
-__device__ __forceinline__ void phase_exact_fixup(float2 (&v)[32], uint32_t ex, float2 *__restrict__ wk, int lane,
-                                                  const PulseParams &pr, const float2 *grow, KB kb_of, long long n,
-                                                  double fc, double fs_over_n) {
+template <bool DISTORT, class GOF, class KB>
+__device__ __forceinline__ void phase_exact_fixup_g(float2 (&v)[32], uint32_t ex, float2 *__restrict__ wk, int lane,
+                                                    const PulseParams &pr, GOF g_of, KB kb_of, long long n,
+                                                    double fc, double fs_over_n) {
   if (!__any_sync(0xffffffffu, ex != 0u)) return;
   __syncwarp();
 #pragma unroll
@@ -67,7 +67,7 @@ __device__ __forceinline__ void phase_exact_fixup(float2 (&v)[32], uint32_t ex, 
   while (ex != 0u) {
     const int s = __ffs(ex) - 1;
     ex &= ex - 1u;
-    const float2 g = grow[lane + 32 * s];
+    const float2 g = g_of(s);
     const long long k = kb_of(s);
     float d = phase_frac_exact(pr.k2, fc, fs_over_n, k >= n / 2 ? k - n : k) - phase_frac(pr.nu_hi, pr.nu_lo, g);
     d -= rintf(d);
@@ -77,6 +77,14 @@ __device__ __forceinline__ void phase_exact_fixup(float2 (&v)[32], uint32_t ex, 
   __syncwarp();
 #pragma unroll
   for (int s = 0; s < 32; ++s) v[s] = wk[wpad(lane + 32 * s)];
+}
+
+// the common case: element s of this lane reads its g entry at grow[lane + 32 s]
+template <bool DISTORT, class KB>
+__device__ __forceinline__ void phase_exact_fixup(float2 (&v)[32], uint32_t ex, float2 *__restrict__ wk, int lane,
+                                                  const PulseParams &pr, const float2 *grow, KB kb_of, long long n,
+                                                  double fc, double fs_over_n) {
+  phase_exact_fixup_g<DISTORT>(v, ex, wk, lane, pr, [&](int s) { return grow[lane + 32 * s]; }, kb_of, n, fc, fs_over_n);
 }
 
 struct WarpArgs {

@@ -12,7 +12,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-COMPONENTS = ["iono8", "iono10", "iono12", "iono14", "iono20", "iono22", "iono24", "doppler", "expand", "compress",
+COMPONENTS = ["iono7", "iono8", "iono9", "iono10", "iono12", "iono14", "iono20", "iono22", "iono24", "doppler", "expand", "compress",
               "fused", "pq", "host"]
 
 

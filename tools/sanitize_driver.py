@@ -1,6 +1,6 @@
 """One small launch of every libdispcorr kernel, for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck).  Run:  compute-sanitizer --tool memcheck python tools/sanitize_driver.py
-Kernels exercised (by plan regime / path): tile_fft (n = 256), warp_row SMALL (n = 1024), warp_small
+Kernels exercised (by plan regime / path): warp_tiny (n = 128 .. 512), tile_fft, warp_row SMALL (n = 1024), warp_small
 (n = 4096), thread_col + warp_row ROWB (n = 2^14), warp_col3 + warp_row ROWB (n = 2^20), warp_col3 +
 tile_fft ROWB (n = 2^22), tile_fft for all passes (n = 2^24), doppler_pipe (first / second order,
 Kaiser), doppler_exact, expand_params (batch > 4096), pulse compression (reference + compress),
@@ -41,7 +41,7 @@ def run_correct(n, batch, W=32, alphas=None, kaiser=0.0, fc=0.0):
     return p
 
 
-for log2n, batch in ((8, 3), (10, 3), (12, 3), (14, 2), (20, 1), (22, 1), (24, 1)):
+for log2n, batch in ((7, 9), (8, 3), (9, 5), (10, 3), (12, 3), (14, 2), (20, 1), (22, 1), (24, 1)):
     if want(f"iono{log2n}"):
         run_correct(1 << log2n, batch)
 if want("doppler"):
