@@ -53,9 +53,10 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) 
   a.ref = f.ref;
   a.ref_idx = f.ref_idx;
   a.ref_out = f.ref_out;
-  // n = 2^20: pass B and pass C both warp-level -- the conj outer twiddle moves from the compute-bound row
-  // pass to the memory-bound column pass (applied on load)
-  const bool outer_c = P1 == 10 && P2 == 10 && f.tw1024 && f.gtab;
+  // warp row pass with a warp-level (n = 2^20) or thread-per-column (2^14 .. 2^16) pass C: the conj outer
+  // twiddle moves from the compute-bound row pass to the memory-bound column pass (applied on load):
+  // row pass 246 -> 267 GS/s at 2^20, 252 -> 272 at 2^16 (stage +1.2 % / +3 %)
+  const bool outer_c = (P1 == 10 || P1 <= 6) && P2 == 10 && f.tw1024 && f.gtab;
   switch (pass) {
     case 0:
       a.src = f.src;
@@ -84,7 +85,11 @@ cudaError_t launch_iono_fourstep_pass(const FourStepArgs &f, int pass, int var) 
         w.outer_c = outer_c;
         return launch_warp_col(w, true, f.stream, f.grid_cap);
       }
-      if (P1 <= 6) return launch_tcol(warp_args(a, f.tw1024), P1, true, f.stream, f.grid_cap);
+      if (P1 <= 6) {
+        WarpArgs w = warp_args(a, f.tw1024);
+        w.outer_c = outer_c;
+        return launch_tcol(w, P1, true, f.stream, f.grid_cap);
+      }
       return launch_col<MODE_COLC>(P1, a, f.stream, f.grid_cap);
     default: return cudaErrorInvalidValue;
   }

@@ -140,6 +140,18 @@ __global__ void __launch_bounds__(kTcolT, 1) thread_col_kernel(const WarpArgs a)
     float2 v[N1];
 #pragma unroll
     for (int r = 0; r < N1; ++r) v[r] = INV ? __ldcg(src + 1024 * r) : __ldcs(src + 1024 * r);
+    if (INV && a.outer_c) {
+      // pass B's conj outer twiddle w_n^(-k1 t2), applied on load (the row pass is the compute-bound one)
+      uint32_t tz;
+      asm volatile("mov.u32 %0, 0;\n" : "=r"(tz));
+      tz += t2;
+#pragma unroll
+      for (int h = 0; h < N1 / 8; ++h) {
+        const float2 hi = twn((uint32_t)(8 * h) * tz & nmask, log2n);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[8 * h + c] = cmulc(v[8 * h + c], cmul(hi, twn((uint32_t)c * tz & nmask, log2n)));
+      }
+    }
     dft_thread<N1, INV>(v);
     if constexpr (!INV) {
       // w_n^(k1 t2) / n = hi(k1 >> 3) lo(k1 & 7); an opaque zero keeps the compiler from hoisting
