@@ -628,3 +628,21 @@ def test_correct_host_fused_small_matches_device(dc):
     yh = np.empty_like(x)
     p.correct_host(x, yh, tec, alpha)
     assert np.array_equal(from_dev(yd), yh)
+
+
+def test_doppler_hann_full_size_sampled(dc):
+    # Hann window on the C3/C4 pulse length, sampled outputs (the taper path of the T = 256 kernel)
+    import torch
+    n = 1 << 20
+    x = synth.complex_gaussian(n, seed=93, batch=2).astype(np.complex64)
+    alphas = [O.alpha_from_velocity(4000.0), O.alpha_from_velocity(-2500.0)]
+    p = dc.Plan(n, 2.048e9, 0.0, taps=32)
+    p.set_window("hann")
+    xd = to_dev(x)
+    yd = torch.empty_like(xd)
+    p.doppler(xd, yd, alphas)
+    y = from_dev(yd)
+    idx = np.unique(np.concatenate([[0, 1, n - 1], np.random.default_rng(4).integers(0, n, 200)]))
+    for i, a in enumerate(alphas):
+        ref = O.doppler_at(x[i].astype(np.complex128), 32, 2.048e9, 0.0, a, idx, kaiser=O.HANN)
+        assert rel_l2(y[i][idx], ref).max() < TOL

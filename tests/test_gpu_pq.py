@@ -183,3 +183,36 @@ def test_pq_all_identity_batch_is_a_copy(dc):
     p.doppler_pq(xd, yd, alphas)
     assert np.array_equal(from_dev(yd), x)
     assert p.info()["kernel_launches"] == l0  # a device copy, no kernels
+
+
+def test_pq_full_size_baseband_carrier_sampled(dc):
+    # 2^20 samples at fs = 204.8 MHz around fc = 422 MHz: the R10 carrier with beta_eff = n / M on sampled
+    # outputs, M = n +- 2j for |v| up to 5 km/s
+    n, fs, fc = 1 << 20, 204.8e6, 422e6
+    vs = [4800.0, -3000.0]
+    x = synth.complex_gaussian(n, seed=91, batch=len(vs)).astype(np.complex64)
+    alphas = [O.alpha_from_velocity(v) for v in vs]
+    assert all(O.pq_length(n, a) != n for a in alphas)
+    y = gpu_pq(dc, x, alphas, fs=fs, fc=fc)
+    idx = np.unique(np.concatenate([[0, 1, n // 3, n - 40], np.random.default_rng(3).integers(0, n - 40, 60)]))
+    for i, a in enumerate(alphas):
+        ref = O.doppler_pq_at(x[i].astype(np.complex128), fs, fc, a, idx)
+        M = O.pq_length(n, a)
+        keep = idx < min(n, M)
+        check(y[i][idx[keep]], ref[keep])
+
+
+def test_pq_plan_reuse_and_stream_order(dc):
+    # one plan, consecutive calls with different M sets (table cache hits and rebuilds), results equal a
+    # fresh plan's
+    import torch
+    n = 1 << 14
+    x = synth.complex_gaussian(n, seed=92, batch=3).astype(np.complex64)
+    sets = [[alpha_for(n, 2), alpha_for(n, -4), 1.0], [alpha_for(n, 6), alpha_for(n, 2), alpha_for(n, -4)]]
+    p = dc.Plan(n, 2.048e9, 0.0, taps=8)
+    xd = to_dev(x)
+    for al in sets:
+        yd = torch.empty_like(xd)
+        p.doppler_pq(xd, yd, al)
+        fresh = gpu_pq(dc, x, al)
+        assert np.array_equal(from_dev(yd), fresh)
