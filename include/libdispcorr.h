@@ -149,7 +149,7 @@ dc_status dc_set_window(dc_plan_t plan, int kind, double param);
  * result in y (must not overlap x).  Pulses run in launch groups of <= 2 GiB; the
  * ionospheric result of a group is kept in a plan-owned device buffer (allocated on the
  * first call, sized to min(batch, group)) between the stages -- except for single-CTA pulses
- * (n = 2^11 .. 2^13) with W = 16 or 32, the rectangular window and |1/alpha - 1| within the
+ * (n = 2^10 .. 2^13) with W = 16 or 32, the rectangular window and |1/alpha - 1| within the
  * first/second-order range, where one fused kernel reads x and writes y once (16 B/sample). */
 dc_status dc_correct(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *tec,
                      const double *alpha);
@@ -180,7 +180,7 @@ dc_status dc_plan_info(dc_plan_t plan, dc_plan_info_t *info);
  * samples processed since the last reset.  Classes: DC_K_IONO_SMALL (regime-0 fused FFT ->
  * phase -> IFFT), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler),
  * DC_K_PQ (one record per dc_doppler_pq launch group: all of its kernels), DC_K_CORRECT_FUSED (the
- * single-round-trip dc_correct kernel of single-CTA pulses: n = 2^11 .. 2^13, W = 16 or 32, no taper). */
+ * single-round-trip dc_correct kernel of short pulses: n = 2^10 .. 2^13, W = 16 or 32, no taper). */
 enum { DC_K_IONO_SMALL = 0, DC_K_FOURSTEP_A = 1, DC_K_FOURSTEP_B = 2, DC_K_FOURSTEP_C = 3, DC_K_DOPPLER = 4,
        DC_K_PQ = 5, DC_K_CORRECT_FUSED = 6, DC_K_CLASSES = 7 };
 typedef struct {

@@ -56,7 +56,7 @@ struct IonoSmallArgs {
 // 3 forward spectra stored conjugated to `ref_out` (no inverse transform)
 cudaError_t launch_iono_small(const IonoSmallArgs &a, int var);
 // fused single-round-trip dc_correct (iono + first/second-order Doppler in one kernel, NEXT-1) for
-// single-CTA pulses: n = 2^11 .. 2^13 and W in {16, 32} (correct_small_supported)
+// short pulses: n = 2^10 (warp-level FFT) and 2^11 .. 2^13 (tile FFT), W in {16, 32} (correct_small_supported)
 bool correct_small_supported(int log2n, int W);
 cudaError_t launch_correct_small(const IonoSmallArgs &a, float2 *y, double carrier, int W, bool second);
 

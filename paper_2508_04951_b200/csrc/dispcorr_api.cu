@@ -427,8 +427,8 @@ dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
   return DC_OK;
 }
 
-// dc_correct of one launch group: the fused single-round-trip kernel where it exists (single-CTA pulses,
-// n = 2^11 .. 2^13, W in {16, 32}, rectangular window, first/second-order Doppler path; NEXT-1), else
+// dc_correct of one launch group: the fused single-round-trip kernel where it exists (short pulses,
+// n = 2^10 .. 2^13, W in {16, 32}, rectangular window, first/second-order Doppler path; NEXT-1), else
 // the ionospheric stage into the group buffer followed by the Doppler stage
 bool correct_fused_ok(const dc_plan_s *p, double max_abs_beta_m1) {
   const int path = dc::doppler_path(max_abs_beta_m1, p->taper, p->taps);

@@ -7,6 +7,7 @@
 #include "tcol.cuh"
 #include "wsmall.cuh"
 #include "wtiny.cuh"
+#include "wcorrect.cuh"
 #include "tma_host.h"
 
 #include <algorithm>

@@ -136,7 +136,19 @@ static cudaError_t launch_correct_small_p(const TileArgs &a, int W, bool second,
   return cudaErrorInvalidValue;
 }
 
-bool correct_small_supported(int log2n, int W) { return log2n >= 11 && log2n <= 13 && (W == 16 || W == 32); }
+template <int W, bool SECOND>
+static cudaError_t launch_correct1024_w(const WarpArgs &a, float2 *y, double carrier, cudaStream_t st, int cap) {
+  auto kern = warp_correct1024_kernel<W, SECOND>;
+  const size_t smem = wcorrect_smem_bytes<W>();
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, kWcNW * 32, smem, &ls);
+  if (e != cudaSuccess) return e;
+  int64_t grid = std::min<int64_t>((a.pulses + kWcNW - 1) / kWcNW, (int64_t)ls.sms * ls.per_sm);
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWcNW * 32), smem, st, a, y, carrier);
+}
+
+bool correct_small_supported(int log2n, int W) { return log2n >= 10 && log2n <= 13 && (W == 16 || W == 32); }
 
 cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carrier, int W, bool second) {
   TileArgs a{};
@@ -154,6 +166,14 @@ cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carri
   a.fc = s.fc;
   a.dop_y = y;
   a.dop_carrier = carrier;
+  if (s.log2n == 10) {  // warp-level FFT, one warp per pulse (wcorrect.cuh)
+    if (!s.tw1024 || !s.gtab) return cudaErrorInvalidValue;
+    const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
+    if (W == 16) return second ? launch_correct1024_w<16, true>(w, y, carrier, s.stream, s.grid_cap)
+                               : launch_correct1024_w<16, false>(w, y, carrier, s.stream, s.grid_cap);
+    return second ? launch_correct1024_w<32, true>(w, y, carrier, s.stream, s.grid_cap)
+                  : launch_correct1024_w<32, false>(w, y, carrier, s.stream, s.grid_cap);
+  }
   switch (s.log2n) {
     case 11: return launch_correct_small_p<11>(a, W, second, s.stream, s.grid_cap);
     case 12: return launch_correct_small_p<12>(a, W, second, s.stream, s.grid_cap);

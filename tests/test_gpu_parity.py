@@ -567,7 +567,7 @@ def test_correct_c3_physics_dilated_dispersed_echo(dc):
 
 
 # ----------------------------------------------------------------------------- fused single-round-trip dc_correct (NEXT-1)
-@pytest.mark.parametrize("log2n", [11, 12, 13])
+@pytest.mark.parametrize("log2n", [10, 11, 12, 13])
 @pytest.mark.parametrize("W", [16, 32])
 @pytest.mark.parametrize("case", ["fast1", "second"])
 def test_correct_fused_small_vs_oracle(dc, log2n, W, case):

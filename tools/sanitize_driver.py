@@ -64,6 +64,7 @@ if want("compress"):
         p.sync()
 if want("fused"):
     run_correct(1 << 12, 5, W=32)                                  # fused single-round-trip dc_correct
+    run_correct(1 << 10, 7, W=32)                                  # fused, warp-level FFT (n = 1024)
     run_correct(1 << 13, 2, W=16, alphas=[1 + 4e-4, 1 - 4e-4], fc=422e6)
 if want("pq"):
     for n in (256, 1 << 14, 1 << 20):                              # tile / four-step regimes of n and 2n
