@@ -815,24 +815,45 @@ dc_status dc_doppler_pq(dc_plan_t p, const void *x, void *y, int64_t batch, cons
   DC_DEVICE_GUARD(p);
   // ---- lazily built state: inner plan of size 2n, table cache, group buffers, staging
   if (!p->pq) {
+    // all-or-nothing: on any failure everything allocated here is released and p->pq stays null
     dc_plan_t inner = nullptr;
     if ((s = dc_plan(&inner, L, p->fs, 0.0, 2, p->device, p->stream)) != DC_OK) return s;
-    p->pq = inner;
-    p->pq_group = std::max<int64_t>(1, std::min<int64_t>(4096, (1ll << 30) / (n * (int64_t)sizeof(float2))));
-    p->pq_cap = (int)std::max<int64_t>(2, std::min<int64_t>(64, (1ll << 30) / (L * (int64_t)sizeof(float2))));
-    const size_t tab_bytes = (size_t)p->pq_cap * L * sizeof(float2);
-    if (cudaMalloc(&p->pq_tabs, tab_bytes) != cudaSuccess ||
-        cudaMalloc(&p->pq_X, (size_t)(p->pq_group * n) * sizeof(float2)) != cudaSuccess ||
-        cudaMalloc(&p->pq_a, (size_t)(p->pq_group * L) * sizeof(float2)) != cudaSuccess ||
-        cudaMalloc(&p->pq_zero, (size_t)p->pq_group * sizeof(PulseParams)) != cudaSuccess) {
+    const int64_t group = std::max<int64_t>(1, std::min<int64_t>(4096, (1ll << 30) / (n * (int64_t)sizeof(float2))));
+    const int cap = (int)std::max<int64_t>(2, std::min<int64_t>(64, (1ll << 30) / (L * (int64_t)sizeof(float2))));
+    const size_t tab_bytes = (size_t)cap * L * sizeof(float2);
+    float2 *tabs = nullptr, *X = nullptr, *A = nullptr;
+    PulseParams *zero = nullptr;
+    cudaEvent_t done = nullptr;
+    auto release = [&]() {
+      for (void *b : {(void *)tabs, (void *)X, (void *)A, (void *)zero})
+        if (b) cudaFree(b);
+      if (done) cudaEventDestroy(done);
+      dc_plan_destroy(inner);
       cudaGetLastError();
+    };
+    if (cudaMalloc(&tabs, tab_bytes) != cudaSuccess || cudaMalloc(&X, (size_t)(group * n) * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&A, (size_t)(group * L) * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&zero, (size_t)group * sizeof(PulseParams)) != cudaSuccess) {
+      release();
       return fail(DC_ERR_OUT_OF_MEMORY, "FFT P/Q buffers");
     }
-    DC_CUDA(cudaMemsetAsync(p->pq_tabs, 0, tab_bytes, p->stream), "cudaMemsetAsync");
-    DC_CUDA(cudaMemsetAsync(p->pq_zero, 0, (size_t)p->pq_group * sizeof(PulseParams), p->stream), "cudaMemsetAsync");
-    DC_CUDA(cudaEventCreateWithFlags(&p->pq_done, cudaEventDisableTiming), "cudaEventCreate");
-    p->pq_tab_M.assign((size_t)p->pq_cap, 0);
-    p->pq_tab_use.assign((size_t)p->pq_cap, 0);
+    cudaError_t e = cudaMemsetAsync(tabs, 0, tab_bytes, p->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(zero, 0, (size_t)group * sizeof(PulseParams), p->stream);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      release();
+      return cuda_fail(e, "FFT P/Q setup");
+    }
+    p->pq = inner;
+    p->pq_group = group;
+    p->pq_cap = cap;
+    p->pq_tabs = tabs;
+    p->pq_X = X;
+    p->pq_a = A;
+    p->pq_zero = zero;
+    p->pq_done = done;
+    p->pq_tab_M.assign((size_t)cap, 0);
+    p->pq_tab_use.assign((size_t)cap, 0);
   }
   p->pq->stream = p->stream;
   if (p->pq_used) DC_CUDA(cudaEventSynchronize(p->pq_done), "cudaEventSynchronize(P/Q staging)");
