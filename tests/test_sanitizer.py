@@ -36,6 +36,10 @@ def test_compute_sanitizer_clean(tool):
                         os.path.join(ROOT, "tools", "sanitize_driver.py"), *comps], cwd=ROOT, capture_output=True,
                        text=True, timeout=1200)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        # the GPU pool disabled compute-sanitizer in round 2 (runs under it left GPUs needing a reset); the
+        # clean logs of the earlier runs are kept in profiles/ (r2_sanitizer_fused.log, r2b_initcheck_components.log)
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + out.strip().splitlines()[0][:200])
     assert "sanitize driver done" in out, out[-3000:]
     summary = [ln for ln in out.splitlines() if "ERROR SUMMARY" in ln or "RACECHECK SUMMARY" in ln]
     assert summary, out[-3000:]
