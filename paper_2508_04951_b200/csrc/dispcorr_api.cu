@@ -569,7 +569,7 @@ dc_status dc_plan(dc_plan_t *out, int64_t n, double fs_hz, double fc_hz, int tap
     if ((s = upload(&p->tw_small_i, build_pass_tables(d, true))) != DC_OK) return cleanup(s);
     if (p->log2n == 10 && d.npass == 2 && d.log_radix_fwd[0] == 5 && d.log_radix_fwd[1] == 5)
       p->tw1024 = p->tw_small_f + dc::tw1024_offset();
-    if (p->log2n >= 12 && p->log2n <= 13) {  // n = N1 x 1024 on the warp FFT (wsmall.cuh)
+    if (p->log2n >= 11 && p->log2n <= 13) {  // n = N1 x 1024 on the warp FFT (wsmall.cuh)
       dc::PlanDesc d10;
       dc::describe_small_plan(10, d10);
       if (d10.npass == 2 && d10.log_radix_fwd[0] == 5 && d10.log_radix_fwd[1] == 5) {

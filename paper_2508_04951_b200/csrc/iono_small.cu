@@ -35,17 +35,16 @@ static cudaError_t launch_small_p(const TileArgs &a, int var, cudaStream_t st, i
 }
 
 template <int N1>
-static cudaError_t launch_wsmall(const WarpArgs &a, int var, cudaStream_t st, int cap) {
-  auto kern = (var == VAR_DISTORT) ? warp_small_kernel<N1, VAR_DISTORT> : warp_small_kernel<N1, VAR_CORRECT>;
-  const size_t smem = wsmall_smem_bytes();
+static cudaError_t launch_wsmall3(const WarpArgs &a, int var, cudaStream_t st, int cap) {
+  auto kern = (var == VAR_DISTORT) ? warp_small3_kernel<N1, VAR_DISTORT> : warp_small3_kernel<N1, VAR_CORRECT>;
+  const size_t smem = wsmall3_smem_bytes();
   LaunchShape ls;
-  cudaError_t e = launch_shape(kern, kWsT, smem, &ls);
+  cudaError_t e = launch_shape(kern, kWs3T, smem, &ls);
   if (e != cudaSuccess) return e;
-  const int sms = ls.sms;
   const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
-  int64_t grid = std::min<int64_t>(tiles, sms);
+  int64_t grid = std::min<int64_t>(tiles, ls.sms);
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWsT), smem, st, a);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWs3T), smem, st, a);
 }
 
 template <int Q>
@@ -87,12 +86,16 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
     if (s.log2n == 8) return launch_wtiny<8>(w, var, s.stream, s.grid_cap);
     return launch_wtiny<16>(w, var, s.stream, s.grid_cap);
   }
-  // in-CTA four-step on the warp FFT (wsmall.cuh) for 4096 / 8192: +5 % / +18 % over the tile
-  // kernel; for 2048 the tile kernel is faster (128 vs 148 GS/s measured) and stays.  Pulse
-  // compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).
-  if (s.log2n >= 12 && s.log2n <= 13 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
+  // in-CTA four-step on the warp FFT (wsmall.cuh) for 2048 .. 8192 (two warp groups, three slots):
+  // 158 / 156 / 169 GS/s vs 154 (tile kernel) / 135 / 137 (one 8-warp group, two buffers) measured.
+  // Pulse compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).
+#ifndef DC_WSMALL3
+#define DC_WSMALL3 1
+#endif
+  if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 13 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
     const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
-    return (s.log2n == 12) ? launch_wsmall<4>(w, var, s.stream, s.grid_cap) : launch_wsmall<8>(w, var, s.stream, s.grid_cap);
+    if (s.log2n == 11) return launch_wsmall3<2>(w, var, s.stream, s.grid_cap);
+    return (s.log2n == 12) ? launch_wsmall3<4>(w, var, s.stream, s.grid_cap) : launch_wsmall3<8>(w, var, s.stream, s.grid_cap);
   }
   switch (s.log2n) {
     case 1: return launch_small_p<1>(a, var, s.stream, s.grid_cap);

@@ -2,15 +2,13 @@
 // n = N1 x 1024 samples, N1 = 2, 4, 8 (n = 2^11 .. 2^13): one HBM round trip per pulse, the
 // four-step decomposition t = 1024 t1 + t2, k = k1 + N1 k2 done entirely in shared memory.
 //
-// A CTA (8 warps) owns tiles of 8192 contiguous samples (8 / N1 whole pulses), double-buffered:
-// the next tile streams in with one bulk copy (cp.async.bulk + transaction mbarrier) while the
-// current one computes.  Per tile:
+// Tiles of 8192 contiguous samples (8 / N1 whole pulses) arrive with one bulk copy each
+// (cp.async.bulk + transaction mbarrier).  Per tile:
 //   A  thread per column (pulse, t2): N1-point DFT over t1 in registers, x w_n^(k1 t2) / n, in place
-//   B  warp per row (pulse, k1): 1024-point forward DFT (wfft1024), the Eq. 15 phase of bin
-//      k1 + N1 k2 (FP32-pair nu from the plan's row-layout 1/f table), inverse DFT,
-//      x conj w_n^(k1 t2), in place
+//   B  warp per row (pulse, k1): 1024-point forward DFT, the Eq. 15 phase of bin k1 + N1 k2
+//      (FP32-pair nu from the plan's row-layout 1/f table), inverse DFT, x conj w_n^(k1 t2), in place
 //   C  thread per column: inverse N1-point DFT over k1, stored straight to y (coalesced rows)
-// The arithmetic is the three-pass four-step of iono_kernels.cu with the intermediate kept in
+// The arithmetic is the three-pass four-step of the n > 8192 regime with the intermediate kept in
 // shared memory, so it matches the warp row pass bit for bit in the row stage.
 #pragma once
 #include "tma.cuh"
@@ -18,13 +16,49 @@
 
 namespace dc {
 
-constexpr int kWsT = 8 * 32;  // threads per CTA
-__host__ __device__ constexpr size_t wsmall_smem_bytes() {
-  return (size_t)2 * 8192 * 8 + (size_t)8 * (kWPad + 32) * 8 + 512 * 16 + 2 * 8 + 128;
+// Two consumer groups of kWs3GW warps, three staging slots (the column-pass pipeline of
+// warp_col3_kernel applied to whole pulses).  Local tile i (8192 contiguous samples = 8 / N1 pulses)
+// goes to group i mod 2 and slot i mod 3; phases A / B / C are separated by the GROUP's named barrier
+// only, so the two groups run out of phase and one group's barrier waits are covered by the other's
+// work, while the third slot streams in.  The warp FFT's exchange space is the row itself (XOR-swizzled
+// in place: wfft1024_ip), so the CTA needs 3 x 64 KiB and no per-warp exchange buffers.  Arithmetic
+// identical to warp_small_kernel (same DFTs, twiddles, phase and rounding order).
+#ifndef DC_WS3_GW
+#define DC_WS3_GW 8
+#endif
+constexpr int kWs3GW = DC_WS3_GW;      // warps per consumer group
+constexpr int kWs3GT = kWs3GW * 32;    // threads per group
+constexpr int kWs3T = 2 * kWs3GT;      // threads per CTA
+__host__ __device__ constexpr size_t wsmall3_smem_bytes() {
+  return (size_t)3 * 8192 * 8 + (size_t)2 * kWs3GW * 32 * 8 + 512 * 16 + 1024 * 8 + 3 * 8 + 128;
+}
+
+// physical slot of logical element i = 32 row + col of a 1024-sample row: 32 row + (col ^ row) --
+// lane-distinct banks both for the Stockham write (row = lane) and the transposed read (col = lane)
+__device__ __forceinline__ int wxor(int i) { return (i & ~31) | ((i ^ (i >> 5)) & 31); }
+
+// wfft1024 with the exchange in the row's own 1024 slots (the caller has every sample in registers)
+template <bool INV>
+__device__ __forceinline__ void wfft1024_ip(float2 (&v)[32], float2 *__restrict__ row, const float4 *__restrict__ tw,
+                                            int lane) {
+  DFT<32, INV>::run(v);
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < 32; ++s) row[wxor(lane * 32 + s)] = v[s];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 32; ++r) v[r] = row[wxor(lane + 32 * r)];
+#pragma unroll
+  for (int h = 0; h < 16; ++h) {
+    const float4 p = tw[h * 32 + lane];
+    if (h > 0) v[2 * h] = INV ? cmulc(v[2 * h], make_float2(p.x, p.y)) : cmul(v[2 * h], make_float2(p.x, p.y));
+    v[2 * h + 1] = INV ? cmulc(v[2 * h + 1], make_float2(p.z, p.w)) : cmul(v[2 * h + 1], make_float2(p.z, p.w));
+  }
+  DFT<32, INV>::run(v);
 }
 
 template <int N1, int VAR>
-__global__ void __launch_bounds__(kWsT, 1) warp_small_kernel(const WarpArgs a) {
+__global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   static_assert(N1 == 2 || N1 == 4 || N1 == 8, "n = 2^11 .. 2^13");
   constexpr int P1 = (N1 == 2) ? 1 : (N1 == 4) ? 2 : 3;
@@ -33,70 +67,68 @@ __global__ void __launch_bounds__(kWsT, 1) warp_small_kernel(const WarpArgs a) {
   constexpr uint32_t nmask = n - 1u;
   constexpr int PPT = 8 / N1;  // pulses per tile
   extern __shared__ __align__(128) float4 smem4[];
-  float2 *bufs = reinterpret_cast<float2 *>(smem4);  // 2 x 8192 samples
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float2 *wk = bufs + 2 * 8192 + warp * kWPad;
-  float2 *Pw = bufs + 2 * 8192 + 8 * kWPad + warp * 32;
-  float4 *Tw = reinterpret_cast<float4 *>(bufs + 2 * 8192 + 8 * (kWPad + 32));
-  uint64_t *bars = reinterpret_cast<uint64_t *>(Tw + 512);
+  float2 *slots = reinterpret_cast<float2 *>(smem4);  // 3 x 8192 samples
+  const int tid = threadIdx.x, grp = tid / kWs3GT, gtid = tid - grp * kWs3GT, warp = gtid >> 5, lane = tid & 31;
+  float2 *Pw = slots + 3 * 8192 + (grp * kWs3GW + warp) * 32;
+  float4 *Tw = reinterpret_cast<float4 *>(slots + 3 * 8192 + 2 * kWs3GW * 32);
+  float2 *T1 = reinterpret_cast<float2 *>(Tw + 512);  // w_n^t2, t2 < 1024 (pass A's column twiddle)
+  uint64_t *full = reinterpret_cast<uint64_t *>(T1 + 1024);
   const int64_t tiles = (a.pulses + PPT - 1) / PPT;
-  for (int i = tid; i < 512; i += kWsT) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
-  auto stage = [&](int64_t t, int b) {  // thread 0: the tile's valid pulses, one bulk copy
-    const int64_t p0 = t * PPT;
+  auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+  for (int i = tid; i < 512; i += kWs3T) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
+  for (int i = tid; i < 1024; i += kWs3T) T1[i] = twn((uint32_t)i, log2n);
+  auto stage = [&](int64_t i) {  // one thread; every generic access to the slot is ordered before it
+    const int64_t p0 = tile_of(i) * PPT;
     const int np = (int)min((int64_t)PPT, a.pulses - p0);
     const unsigned bytes = (unsigned)(np * n * sizeof(float2));
-    mbar_arrive_expect_tx(&bars[b], bytes);
-    bulk_load(bufs + b * 8192, a.src + p0 * (int64_t)n, bytes, &bars[b]);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[i % 3], bytes);
+    bulk_load(slots + (i % 3) * 8192, a.src + p0 * (int64_t)n, bytes, &full[i % 3]);
   };
-  int64_t t = blockIdx.x;
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int s = 0; s < 3; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
-    if (t < tiles) stage(t, 0);
+    for (int64_t i = 0; i < 3; ++i)
+      if (tile_of(i) < tiles) stage(i);
   }
   __syncthreads();
-  unsigned phase[2] = {0u, 0u};
-  for (int b = 0; t < tiles; t += gridDim.x, b ^= 1) {
-    if (tid == 0 && t + gridDim.x < tiles) {
-      fence_proxy_async();  // buffer b ^ 1 was last read by generic loads before the trailing barrier
-      stage(t + gridDim.x, b ^ 1);
-    }
-    mbar_wait(&bars[b], phase[b]);
-    phase[b] ^= 1u;
-    float2 *sb = bufs + b * 8192;
-    const int64_t p0 = t * PPT;
+  auto group_sync = [grp] { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(kWs3GT) : "memory"); };
+
+  for (int64_t i = grp; tile_of(i) < tiles; i += 2) {
+    float2 *sb = slots + (i % 3) * 8192;
+    mbar_wait(&full[i % 3], (unsigned)((i / 3) & 1));
+    const int64_t p0 = tile_of(i) * PPT;
     const int np = (int)min((int64_t)PPT, a.pulses - p0);
     // ---- A: columns (pulse pl, t2), forward N1-point DFT, x w_n^(k1 t2) / n
 #pragma unroll 1
-    for (int c = tid; c < np * 1024; c += kWsT) {
+    for (int c = gtid; c < np * 1024; c += kWs3GT) {
       float2 *col = sb + (c >> 10) * n + (c & 1023);
       const uint32_t t2 = (uint32_t)(c & 1023);
       float2 v[N1];
 #pragma unroll
       for (int r = 0; r < N1; ++r) v[r] = col[1024 * r];
       DFT<N1, false>::run(v);
-      const float2 w1 = twn(t2 & nmask, log2n);
+      const float2 w1 = T1[t2];  // = twn(t2, log2n)
       float2 w = cscale(make_float2(1.f, 0.f), a.scale);
-      const float2 w1s = w1;
 #pragma unroll
       for (int k1 = 0; k1 < N1; ++k1) {
         col[1024 * k1] = cmul(v[k1], w);
-        w = cmul(w, w1s);  // w_n^(k1 t2): at most 7 products of correctly rounded twiddles
+        w = cmul(w, w1);  // w_n^(k1 t2): at most 7 products of correctly rounded twiddles
       }
     }
-    __syncthreads();
+    group_sync();
     // ---- B: rows (pulse pl, k1): forward DFT -> phase -> inverse DFT -> x conj w_n^(k1 t2)
-    if (warp < np * N1) {
-      const int pl = warp / N1, k1 = warp - pl * N1;
+#pragma unroll 1
+    for (int rw = warp; rw < np * N1; rw += kWs3GW) {
+      const int pl = rw / N1, k1 = rw - pl * N1;
       float2 *row = sb + pl * n + 1024 * k1;
       float2 v[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = row[lane + 32 * r];
-      wfft1024<false>(v, wk, Tw, lane);
+      wfft1024_ip<false>(v, row, Tw, lane);
       const PulseParams pr = a.pp[a.pulse_base + p0 + pl];
       const float2 *grow = a.gtab + 1024 * k1;
-      uint32_t ex = 0u;  // elements needing the exact binary64 phase (phase_exact_fixup)
+      uint32_t ex = 0u;  // elements needing the exact binary64 phase
 #pragma unroll
       for (int s = 0; s < 32; ++s) {
         if (s % 8 == 0) asm volatile("" ::: "memory");  // table loads in chunks of 8 (registers)
@@ -105,21 +137,37 @@ __global__ void __launch_bounds__(kWsT, 1) warp_small_kernel(const WarpArgs a) {
         ex |= phase_needs_exact(pr.nu_hi, g) ? (1u << s) : 0u;
         v[s] = cmul(v[s], expm2pi((VAR == VAR_DISTORT) ? -rf : rf));
       }
-      phase_exact_fixup<VAR == VAR_DISTORT>(
-          v, ex, wk, lane, pr, grow, [&](int s) { return (long long)k1 + (long long)N1 * (lane + 32 * s); }, n, a.fc,
-          a.fs_over_n);
-      wfft1024<true>(v, wk, Tw, lane);
+      if (__any_sync(0xffffffffu, ex != 0u)) {  // rare: the exact binary64 phase (phase_exact_fixup_g)
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 32; ++s) row[lane + 32 * s] = v[s];
+#pragma unroll 1
+        while (ex != 0u) {
+          const int s = __ffs(ex) - 1;
+          ex &= ex - 1u;
+          const float2 g = grow[lane + 32 * s];
+          const long long k = (long long)k1 + (long long)N1 * (lane + 32 * s);
+          float d = phase_frac_exact(pr.k2, a.fc, a.fs_over_n, k >= n / 2 ? k - n : k) - phase_frac(pr.nu_hi, pr.nu_lo, g);
+          d -= rintf(d);
+          float2 &e = row[lane + 32 * s];
+          e = cmul(e, expm2pi((VAR == VAR_DISTORT) ? -d : d));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 32; ++s) v[s] = row[lane + 32 * s];
+      }
+      wfft1024_ip<true>(v, row, Tw, lane);
       __syncwarp();
       Pw[lane] = twn((32u * (uint32_t)k1 * (uint32_t)lane) & nmask, log2n);
-      const float2 base = twn(((uint32_t)k1 * (uint32_t)lane) & nmask, log2n);
+      const float2 base = T1[k1 * lane];  // = twn(k1 lane, log2n): k1 lane < 256
       __syncwarp();
 #pragma unroll
       for (int s = 0; s < 32; ++s) row[lane + 32 * s] = cmulc(v[s], cmul(base, Pw[s]));
     }
-    __syncthreads();
+    group_sync();
     // ---- C: columns, inverse N1-point DFT over k1 -> y[1024 t1 + t2]
 #pragma unroll 1
-    for (int c = tid; c < np * 1024; c += kWsT) {
+    for (int c = gtid; c < np * 1024; c += kWs3GT) {
       const int pl = c >> 10;
       const float2 *col = sb + pl * n + (c & 1023);
       float2 v[N1];
@@ -130,7 +178,8 @@ __global__ void __launch_bounds__(kWsT, 1) warp_small_kernel(const WarpArgs a) {
 #pragma unroll
       for (int r = 0; r < N1; ++r) __stcs(yp + 1024 * r, v[r]);
     }
-    __syncthreads();  // buffer b consumed
+    group_sync();  // slot drained: stream tile i + 3 into it
+    if (gtid == 0 && tile_of(i + 3) < tiles) stage(i + 3);
   }
 }
 
