@@ -149,7 +149,9 @@ __device__ __forceinline__ uint32_t dop_membership(double md, double beta, doubl
 // (kDopSeg samples) as ONE bulk async copy issued by lane 0 (no LDS/STG per output, no CTA barrier).
 // TAPER > 0: tapered weights h = sinc K, h' = sinc' K + sinc K' (first-order path only): the Hann window
 // (TAPER == kTaperHann) or a Kaiser window of TAPER series terms.
-template <bool SECOND, int WT, int TAPER = 0, int R = dop_r(WT)>
+// DIRECT: each thread stores its own R outputs (m < n) straight to y -- no staging segment (`ob` unused),
+// for the fused kernels whose shared memory is taken by their FFT tiles.
+template <bool SECOND, int WT, int TAPER = 0, int R = dop_r(WT), bool DIRECT = false>
 __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, const DopTile &cur, int W_rt,
                                                  float2 *__restrict__ ob, float2 *__restrict__ y, int64_t n,
                                                  double carrier, const TaperCoef *tcp = nullptr) {
@@ -301,6 +303,13 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
       const double psi = g * (double)(mt + r);
       acc[r] = cmul(acc[r], expm2pi(__double2float_rn(psi - rint(psi))));
     }
+  }
+  if constexpr (DIRECT) {
+    float2 *yp = y + cur.pulse * n;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (mt + r < n) __stcs(yp + mt + r, acc[r]);
+    return;
   }
   // ---- store: the warp's 32 x R outputs are contiguous (thread t owns [t R, t R + R)).  Lane 0's
   // previous bulk store must have finished reading the segment before it is overwritten.

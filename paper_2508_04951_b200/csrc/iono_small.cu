@@ -17,6 +17,10 @@
 
 namespace dc {
 
+#ifndef DC_WSMALL3
+#define DC_WSMALL3 1  // n = 2^11 .. 2^13 on the in-CTA four-step kernels (0: the tile kernels, for A/B tuning builds)
+#endif
+
 template <int P, int VAR>
 static cudaError_t launch_small_pv(const TileArgs &a, cudaStream_t st, int cap) {
   constexpr int NB = small_nb(P);
@@ -44,7 +48,7 @@ static cudaError_t launch_wsmall3(const WarpArgs &a, int var, cudaStream_t st, i
   const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
   int64_t grid = std::min<int64_t>(tiles, ls.sms);
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWs3T), smem, st, a);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWs3T), smem, st, a, (float2 *)nullptr, 0.0);
 }
 
 template <int Q>
@@ -89,9 +93,6 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   // in-CTA four-step on the warp FFT (wsmall.cuh) for 2048 .. 8192 (two warp groups, three slots):
   // 158 / 156 / 169 GS/s vs 154 (tile kernel) / 135 / 137 (one 8-warp group, two buffers) measured.
   // Pulse compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).
-#ifndef DC_WSMALL3
-#define DC_WSMALL3 1
-#endif
   if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 13 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
     const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
     if (s.log2n == 11) return launch_wsmall3<2>(w, var, s.stream, s.grid_cap);
@@ -151,6 +152,25 @@ static cudaError_t launch_correct1024_w(const WarpArgs &a, float2 *y, double car
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kWcNW * 32), smem, st, a, y, carrier);
 }
 
+template <int N1, int W, bool SECOND>
+static cudaError_t launch_wscorrect(const WarpArgs &a, float2 *y, double carrier, cudaStream_t st, int cap) {
+  auto kern = warp_small3_kernel<N1, VAR_CORRECT, W, SECOND>;
+  const size_t smem = wsmall3_smem_bytes(N1, W);
+  LaunchShape ls;
+  cudaError_t e = launch_shape(kern, kWs3T, smem, &ls);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
+  int64_t grid = std::min<int64_t>(tiles, ls.sms);
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kWs3T), smem, st, a, y, carrier);
+}
+template <int N1>
+static cudaError_t launch_wscorrect_n(const WarpArgs &a, float2 *y, double carrier, int W, bool second, cudaStream_t st,
+                                      int cap) {
+  if (W == 16) return second ? launch_wscorrect<N1, 16, true>(a, y, carrier, st, cap) : launch_wscorrect<N1, 16, false>(a, y, carrier, st, cap);
+  return second ? launch_wscorrect<N1, 32, true>(a, y, carrier, st, cap) : launch_wscorrect<N1, 32, false>(a, y, carrier, st, cap);
+}
+
 bool correct_small_supported(int log2n, int W) { return log2n >= 10 && log2n <= 13 && (W == 16 || W == 32); }
 
 cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carrier, int W, bool second) {
@@ -176,6 +196,13 @@ cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carri
                                : launch_correct1024_w<16, false>(w, y, carrier, s.stream, s.grid_cap);
     return second ? launch_correct1024_w<32, true>(w, y, carrier, s.stream, s.grid_cap)
                   : launch_correct1024_w<32, false>(w, y, carrier, s.stream, s.grid_cap);
+  }
+  // n = 2^11 .. 2^13: the in-CTA four-step kernel with the Doppler stage on its slots (wsmall.cuh)
+  if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 13 && s.tw1024 && s.gtab) {
+    const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
+    if (s.log2n == 11) return launch_wscorrect_n<2>(w, y, carrier, W, second, s.stream, s.grid_cap);
+    if (s.log2n == 12) return launch_wscorrect_n<4>(w, y, carrier, W, second, s.stream, s.grid_cap);
+    return launch_wscorrect_n<8>(w, y, carrier, W, second, s.stream, s.grid_cap);
   }
   switch (s.log2n) {
     case 11: return launch_correct_small_p<11>(a, W, second, s.stream, s.grid_cap);

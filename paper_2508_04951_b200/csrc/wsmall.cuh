@@ -12,6 +12,7 @@
 // shared memory, so it matches the warp row pass bit for bit in the row stage.
 #pragma once
 #include "tma.cuh"
+#include "doppler_tile.cuh"
 #include "wfft.cuh"
 
 namespace dc {
@@ -29,8 +30,11 @@ namespace dc {
 constexpr int kWs3GW = DC_WS3_GW;      // warps per consumer group
 constexpr int kWs3GT = kWs3GW * 32;    // threads per group
 constexpr int kWs3T = 2 * kWs3GT;      // threads per CTA
-__host__ __device__ constexpr size_t wsmall3_smem_bytes() {
-  return (size_t)3 * 8192 * 8 + (size_t)2 * kWs3GW * 32 * 8 + 512 * 16 + 1024 * 8 + 3 * 8 + 128;
+// slot of 8192 samples; the fused dc_correct variant (DOPW > 0) gives every pulse kCsPad zeros on each
+// side (R12: x = 0 outside [0, n)) for the Doppler stage that runs on the slot after pass C
+__host__ __device__ constexpr int wsmall3_slot(int N1, int dopw) { return 8192 + (dopw ? (8 / N1) * 2 * kCsPad : 0); }
+__host__ __device__ constexpr size_t wsmall3_smem_bytes(int N1 = 8, int dopw = 0) {
+  return (size_t)3 * wsmall3_slot(N1, dopw) * 8 + (size_t)2 * kWs3GW * 32 * 8 + 512 * 16 + 1024 * 8 + 3 * 8 + 128;
 }
 
 // physical slot of logical element i = 32 row + col of a 1024-sample row: 32 row + (col ^ row) --
@@ -57,8 +61,12 @@ __device__ __forceinline__ void wfft1024_ip(float2 (&v)[32], float2 *__restrict_
   DFT<32, INV>::run(v);
 }
 
-template <int N1, int VAR>
-__global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a) {
+// DOPW > 0: fused single-round-trip dc_correct (NEXT-1): pass C leaves the ionospheric result in the
+// slot (zero-margined) and the group resamples it there (Eq. 16, doppler_tile.cuh, W = DOPW, direct
+// stores of R outputs per thread); x is read and y written once, 16 B/sample for both stages.
+template <int N1, int VAR, int DOPW = 0, bool DSECOND = false>
+__global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a, float2 *__restrict__ y = nullptr,
+                                                                double carrier = 0.0) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
   static_assert(N1 == 2 || N1 == 4 || N1 == 8, "n = 2^11 .. 2^13");
   constexpr int P1 = (N1 == 2) ? 1 : (N1 == 4) ? 2 : 3;
@@ -66,24 +74,36 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a)
   constexpr int n = 1 << log2n;
   constexpr uint32_t nmask = n - 1u;
   constexpr int PPT = 8 / N1;  // pulses per tile
-  extern __shared__ __align__(128) float4 smem4[];
-  float2 *slots = reinterpret_cast<float2 *>(smem4);  // 3 x 8192 samples
+  constexpr int PAD = DOPW ? kCsPad : 0, PS = n + 2 * PAD, SLOT = wsmall3_slot(N1, DOPW);  // pulse pl at slot + pl PS + PAD
+  extern __shared__ __align__(1024) float4 smem4[];
+  float2 *slots = reinterpret_cast<float2 *>(smem4);  // 3 x SLOT samples
   const int tid = threadIdx.x, grp = tid / kWs3GT, gtid = tid - grp * kWs3GT, warp = gtid >> 5, lane = tid & 31;
-  float2 *Pw = slots + 3 * 8192 + (grp * kWs3GW + warp) * 32;
-  float4 *Tw = reinterpret_cast<float4 *>(slots + 3 * 8192 + 2 * kWs3GW * 32);
+  float2 *Pw = slots + 3 * SLOT + (grp * kWs3GW + warp) * 32;
+  float4 *Tw = reinterpret_cast<float4 *>(slots + 3 * SLOT + 2 * kWs3GW * 32);
   float2 *T1 = reinterpret_cast<float2 *>(Tw + 512);  // w_n^t2, t2 < 1024 (pass A's column twiddle)
   uint64_t *full = reinterpret_cast<uint64_t *>(T1 + 1024);
   const int64_t tiles = (a.pulses + PPT - 1) / PPT;
   auto tile_of = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
   for (int i = tid; i < 512; i += kWs3T) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
   for (int i = tid; i < 1024; i += kWs3T) T1[i] = twn((uint32_t)i, log2n);
+  if constexpr (PAD > 0) {  // the margins are never written again
+    for (int i = tid; i < 3 * PPT * 2 * PAD; i += kWs3T) {
+      const int sl = i / (PPT * 2 * PAD), j = i - sl * (PPT * 2 * PAD), pl = j / (2 * PAD), e = j - pl * 2 * PAD;
+      slots[sl * SLOT + pl * PS + (e < PAD ? e : n + e)] = make_float2(0.f, 0.f);
+    }
+  }
   auto stage = [&](int64_t i) {  // one thread; every generic access to the slot is ordered before it
     const int64_t p0 = tile_of(i) * PPT;
     const int np = (int)min((int64_t)PPT, a.pulses - p0);
     const unsigned bytes = (unsigned)(np * n * sizeof(float2));
     fence_proxy_async();
     mbar_arrive_expect_tx(&full[i % 3], bytes);
-    bulk_load(slots + (i % 3) * 8192, a.src + p0 * (int64_t)n, bytes, &full[i % 3]);
+    if constexpr (PAD == 0) {
+      bulk_load(slots + (i % 3) * SLOT, a.src + p0 * (int64_t)n, bytes, &full[i % 3]);
+    } else {
+      for (int pl = 0; pl < np; ++pl)
+        bulk_load(slots + (i % 3) * SLOT + pl * PS + PAD, a.src + (p0 + pl) * (int64_t)n, n * sizeof(float2), &full[i % 3]);
+    }
   };
   if (tid == 0) {
     for (int s = 0; s < 3; ++s) mbar_init(&full[s], 1);
@@ -95,14 +115,14 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a)
   auto group_sync = [grp] { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(kWs3GT) : "memory"); };
 
   for (int64_t i = grp; tile_of(i) < tiles; i += 2) {
-    float2 *sb = slots + (i % 3) * 8192;
+    float2 *sb = slots + (i % 3) * SLOT;
     mbar_wait(&full[i % 3], (unsigned)((i / 3) & 1));
     const int64_t p0 = tile_of(i) * PPT;
     const int np = (int)min((int64_t)PPT, a.pulses - p0);
     // ---- A: columns (pulse pl, t2), forward N1-point DFT, x w_n^(k1 t2) / n
 #pragma unroll 1
     for (int c = gtid; c < np * 1024; c += kWs3GT) {
-      float2 *col = sb + (c >> 10) * n + (c & 1023);
+      float2 *col = sb + (c >> 10) * PS + PAD + (c & 1023);
       const uint32_t t2 = (uint32_t)(c & 1023);
       float2 v[N1];
 #pragma unroll
@@ -121,7 +141,7 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a)
 #pragma unroll 1
     for (int rw = warp; rw < np * N1; rw += kWs3GW) {
       const int pl = rw / N1, k1 = rw - pl * N1;
-      float2 *row = sb + pl * n + 1024 * k1;
+      float2 *row = sb + pl * PS + PAD + 1024 * k1;
       float2 v[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = row[lane + 32 * r];
@@ -169,14 +189,38 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a)
 #pragma unroll 1
     for (int c = gtid; c < np * 1024; c += kWs3GT) {
       const int pl = c >> 10;
-      const float2 *col = sb + pl * n + (c & 1023);
+      float2 *col = sb + pl * PS + PAD + (c & 1023);
       float2 v[N1];
 #pragma unroll
       for (int r = 0; r < N1; ++r) v[r] = col[1024 * r];
       DFT<N1, true>::run(v);
-      float2 *yp = a.dst + (p0 + pl) * (int64_t)n + (c & 1023);
+      if constexpr (DOPW > 0) {
 #pragma unroll
-      for (int r = 0; r < N1; ++r) __stcs(yp + 1024 * r, v[r]);
+        for (int r = 0; r < N1; ++r) col[1024 * r] = v[r];
+      } else {
+        float2 *yp = a.dst + (p0 + pl) * (int64_t)n + (c & 1023);
+#pragma unroll
+        for (int r = 0; r < N1; ++r) __stcs(yp + 1024 * r, v[r]);
+      }
+    }
+    if constexpr (DOPW > 0) {
+      // ---- D: Doppler (Eq. 16 windowed, D1-D4) of the tile's pulses from the slot, 32 R outputs per warp
+      // and item; dop_tile_compute places thread t at m0 + t R, so m0 undoes the CTA-wide warp offset
+      constexpr int R = dop_r(DOPW), SEG = 32 * R, NSEG = (n + SEG - 1) / SEG;
+      group_sync();
+#pragma unroll 1
+      for (int q = warp; q < np * NSEG; q += kWs3GW) {
+        const int pl = q / NSEG, sg = q - pl * NSEG;
+        DopTile cur;
+        cur.pulse = p0 + pl;
+        cur.m0 = (int64_t)sg * SEG - (int64_t)(tid >> 5) * SEG;
+        cur.Bcta = -PAD;
+        cur.beta = a.pp[a.pulse_base + p0 + pl].beta;
+        cur.span = 0;
+        cur.pad0 = 0;
+        cur.pad1 = 0;
+        dop_tile_compute<DSECOND, DOPW, 0, R, true>(sb + pl * PS, cur, DOPW, nullptr, y, n, carrier);
+      }
     }
     group_sync();  // slot drained: stream tile i + 3 into it
     if (gtid == 0 && tile_of(i + 3) < tiles) stage(i + 3);
