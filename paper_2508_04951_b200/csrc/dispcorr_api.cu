@@ -377,9 +377,11 @@ struct RefArgs {
   float2 *ref_out = nullptr;
 };
 // var: 0 Eq. 15, 1 Eq. 14, 2 Eq. 15 + matched filter (tables ra.ref), 3 conj spectra into ra.ref_out
+// n = 2^14 (regime 1) runs Eq. 15 / Eq. 14 on the in-CTA four-step kernel (one HBM round trip, wsmall.cuh)
+bool incta_2e14(const dc_plan_s *p) { return p->log2n == 14 && p->tw1024 && p->gtab; }
 dc_status run_iono(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                    int64_t pulse_base, int var, Lane ln, RefArgs ra = RefArgs{}) {
-  if (p->regime == 0) {
+  if (p->regime == 0 || (incta_2e14(p) && (var == 0 || var == 1))) {
     dc::IonoSmallArgs a{src, dst, pulses, p->log2n, pp ? pp + pulse_base : nullptr, p->tw_small_f, p->tw_small_i,
                         p->fs / (double)p->n, p->fc, ln.st, p->tw1024, ln.cap, p->gtab, ra.ref,
                         ra.ref_idx ? ra.ref_idx + pulse_base : nullptr, ra.ref_out};
@@ -428,11 +430,11 @@ dc_status run_doppler(dc_plan_s *p, const float2 *src, float2 *dst, int64_t puls
 }
 
 // dc_correct of one launch group: the fused single-round-trip kernel where it exists (short pulses,
-// n = 2^10 .. 2^13, W in {16, 32}, rectangular window, first/second-order Doppler path; NEXT-1), else
+// n = 2^10 .. 2^14, W in {16, 32}, rectangular window, first/second-order Doppler path; NEXT-1), else
 // the ionospheric stage into the group buffer followed by the Doppler stage
 bool correct_fused_ok(const dc_plan_s *p, double max_abs_beta_m1) {
   const int path = dc::doppler_path(max_abs_beta_m1, p->taper, p->taps);
-  return p->regime == 0 && !p->taper && path != 0 && dc::correct_small_supported(p->log2n, p->taps);
+  return (p->regime == 0 || incta_2e14(p)) && !p->taper && path != 0 && dc::correct_small_supported(p->log2n, p->taps);
 }
 dc_status run_correct(dc_plan_s *p, const float2 *src, float2 *dst, int64_t pulses, const PulseParams *pp,
                       int64_t pulse_base, double max_abs_beta_m1, Lane ln) {

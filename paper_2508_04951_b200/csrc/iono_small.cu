@@ -41,11 +41,11 @@ static cudaError_t launch_small_p(const TileArgs &a, int var, cudaStream_t st, i
 template <int N1>
 static cudaError_t launch_wsmall3(const WarpArgs &a, int var, cudaStream_t st, int cap) {
   auto kern = (var == VAR_DISTORT) ? warp_small3_kernel<N1, VAR_DISTORT> : warp_small3_kernel<N1, VAR_CORRECT>;
-  const size_t smem = wsmall3_smem_bytes();
+  const size_t smem = wsmall3_smem_bytes(N1, 0);
   LaunchShape ls;
   cudaError_t e = launch_shape(kern, kWs3T, smem, &ls);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
+  const int64_t tiles = (a.pulses + wsmall3_ppt(N1) - 1) / wsmall3_ppt(N1);
   int64_t grid = std::min<int64_t>(tiles, ls.sms);
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kWs3T), smem, st, a, (float2 *)nullptr, 0.0);
@@ -93,8 +93,9 @@ cudaError_t launch_iono_small(const IonoSmallArgs &s, int var) {
   // in-CTA four-step on the warp FFT (wsmall.cuh) for 2048 .. 8192 (two warp groups, three slots):
   // 158 / 156 / 169 GS/s vs 154 (tile kernel) / 135 / 137 (one 8-warp group, two buffers) measured.
   // Pulse compression and spectrum output (var 2, 3) run on the tile kernel (natural bin order).
-  if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 13 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
+  if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 14 && s.tw1024 && s.gtab && (var == VAR_CORRECT || var == VAR_DISTORT)) {
     const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
+    if (s.log2n == 14) return launch_wsmall3<16>(w, var, s.stream, s.grid_cap);
     if (s.log2n == 11) return launch_wsmall3<2>(w, var, s.stream, s.grid_cap);
     return (s.log2n == 12) ? launch_wsmall3<4>(w, var, s.stream, s.grid_cap) : launch_wsmall3<8>(w, var, s.stream, s.grid_cap);
   }
@@ -159,7 +160,7 @@ static cudaError_t launch_wscorrect(const WarpArgs &a, float2 *y, double carrier
   LaunchShape ls;
   cudaError_t e = launch_shape(kern, kWs3T, smem, &ls);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = (a.pulses + (8 / N1) - 1) / (8 / N1);
+  const int64_t tiles = (a.pulses + wsmall3_ppt(N1) - 1) / wsmall3_ppt(N1);
   int64_t grid = std::min<int64_t>(tiles, ls.sms);
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kWs3T), smem, st, a, y, carrier);
@@ -171,7 +172,9 @@ static cudaError_t launch_wscorrect_n(const WarpArgs &a, float2 *y, double carri
   return second ? launch_wscorrect<N1, 32, true>(a, y, carrier, st, cap) : launch_wscorrect<N1, 32, false>(a, y, carrier, st, cap);
 }
 
-bool correct_small_supported(int log2n, int W) { return log2n >= 10 && log2n <= 13 && (W == 16 || W == 32); }
+bool correct_small_supported(int log2n, int W) {
+  return log2n >= 10 && log2n <= (DC_WSMALL3 ? 14 : 13) && (W == 16 || W == 32);
+}
 
 cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carrier, int W, bool second) {
   TileArgs a{};
@@ -198,8 +201,9 @@ cudaError_t launch_correct_small(const IonoSmallArgs &s, float2 *y, double carri
                   : launch_correct1024_w<32, false>(w, y, carrier, s.stream, s.grid_cap);
   }
   // n = 2^11 .. 2^13: the in-CTA four-step kernel with the Doppler stage on its slots (wsmall.cuh)
-  if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 13 && s.tw1024 && s.gtab) {
+  if (DC_WSMALL3 && s.log2n >= 11 && s.log2n <= 14 && s.tw1024 && s.gtab) {
     const WarpArgs w = warp_args(a, s.tw1024, s.gtab);
+    if (s.log2n == 14) return launch_wscorrect_n<16>(w, y, carrier, W, second, s.stream, s.grid_cap);
     if (s.log2n == 11) return launch_wscorrect_n<2>(w, y, carrier, W, second, s.stream, s.grid_cap);
     if (s.log2n == 12) return launch_wscorrect_n<4>(w, y, carrier, W, second, s.stream, s.grid_cap);
     return launch_wscorrect_n<8>(w, y, carrier, W, second, s.stream, s.grid_cap);

@@ -17,24 +17,25 @@
 
 namespace dc {
 
-// Two consumer groups of kWs3GW warps, three staging slots (the column-pass pipeline of
+// Two consumer groups of 8 warps, three staging slots (the column-pass pipeline of
 // warp_col3_kernel applied to whole pulses).  Local tile i (8192 contiguous samples = 8 / N1 pulses)
 // goes to group i mod 2 and slot i mod 3; phases A / B / C are separated by the GROUP's named barrier
 // only, so the two groups run out of phase and one group's barrier waits are covered by the other's
 // work, while the third slot streams in.  The warp FFT's exchange space is the row itself (XOR-swizzled
 // in place: wfft1024_ip), so the CTA needs 3 x 64 KiB and no per-warp exchange buffers.  Arithmetic
 // identical to warp_small_kernel (same DFTs, twiddles, phase and rounding order).
-#ifndef DC_WS3_GW
-#define DC_WS3_GW 8
-#endif
-constexpr int kWs3GW = DC_WS3_GW;      // warps per consumer group
-constexpr int kWs3GT = kWs3GW * 32;    // threads per group
-constexpr int kWs3T = 2 * kWs3GT;      // threads per CTA
+constexpr int kWs3T = 512;  // threads per CTA: two 8-warp groups (one 16-warp group at n = 2^14)
 // slot of 8192 samples; the fused dc_correct variant (DOPW > 0) gives every pulse kCsPad zeros on each
 // side (R12: x = 0 outside [0, n)) for the Doppler stage that runs on the slot after pass C
-__host__ __device__ constexpr int wsmall3_slot(int N1, int dopw) { return 8192 + (dopw ? (8 / N1) * 2 * kCsPad : 0); }
+// n = 2^14 (N1 = 16): one pulse is a 128 KiB tile, so the CTA runs ONE 16-warp group on ONE slot (the
+// next pulse streams in once pass C has drained the slot)
+__host__ __device__ constexpr int wsmall3_ppt(int N1) { return N1 >= 8 ? 1 : 8 / N1; }
+__host__ __device__ constexpr int wsmall3_nslot(int N1) { return N1 == 16 ? 1 : 3; }
+__host__ __device__ constexpr int wsmall3_slot(int N1, int dopw) {
+  return (N1 == 16 ? 16384 : 8192) + (dopw ? wsmall3_ppt(N1) * 2 * kCsPad : 0);
+}
 __host__ __device__ constexpr size_t wsmall3_smem_bytes(int N1 = 8, int dopw = 0) {
-  return (size_t)3 * wsmall3_slot(N1, dopw) * 8 + (size_t)2 * kWs3GW * 32 * 8 + 512 * 16 + 1024 * 8 + 3 * 8 + 128;
+  return (size_t)wsmall3_nslot(N1) * wsmall3_slot(N1, dopw) * 8 + (size_t)kWs3T * 8 + 512 * 16 + 1024 * 8 + 3 * 8 + 128;
 }
 
 // physical slot of logical element i = 32 row + col of a 1024-sample row: 32 row + (col ^ row) --
@@ -68,18 +69,19 @@ template <int N1, int VAR, int DOPW = 0, bool DSECOND = false>
 __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a, float2 *__restrict__ y = nullptr,
                                                                 double carrier = 0.0) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
-  static_assert(N1 == 2 || N1 == 4 || N1 == 8, "n = 2^11 .. 2^13");
-  constexpr int P1 = (N1 == 2) ? 1 : (N1 == 4) ? 2 : 3;
+  static_assert(N1 == 2 || N1 == 4 || N1 == 8 || N1 == 16, "n = 2^11 .. 2^14");
+  constexpr int P1 = (N1 == 2) ? 1 : (N1 == 4) ? 2 : (N1 == 8) ? 3 : 4;
   constexpr int log2n = P1 + 10;
   constexpr int n = 1 << log2n;
   constexpr uint32_t nmask = n - 1u;
-  constexpr int PPT = 8 / N1;  // pulses per tile
+  constexpr int PPT = wsmall3_ppt(N1);  // pulses per tile
+  constexpr int NSLOT = wsmall3_nslot(N1), NGRP = (N1 == 16) ? 1 : 2, GT = kWs3T / NGRP, GW = GT / 32;
   constexpr int PAD = DOPW ? kCsPad : 0, PS = n + 2 * PAD, SLOT = wsmall3_slot(N1, DOPW);  // pulse pl at slot + pl PS + PAD
   extern __shared__ __align__(1024) float4 smem4[];
-  float2 *slots = reinterpret_cast<float2 *>(smem4);  // 3 x SLOT samples
-  const int tid = threadIdx.x, grp = tid / kWs3GT, gtid = tid - grp * kWs3GT, warp = gtid >> 5, lane = tid & 31;
-  float2 *Pw = slots + 3 * SLOT + (grp * kWs3GW + warp) * 32;
-  float4 *Tw = reinterpret_cast<float4 *>(slots + 3 * SLOT + 2 * kWs3GW * 32);
+  float2 *slots = reinterpret_cast<float2 *>(smem4);  // NSLOT x SLOT samples
+  const int tid = threadIdx.x, grp = tid / GT, gtid = tid - grp * GT, warp = gtid >> 5, lane = tid & 31;
+  float2 *Pw = slots + NSLOT * SLOT + (tid >> 5) * 32;
+  float4 *Tw = reinterpret_cast<float4 *>(slots + NSLOT * SLOT + kWs3T);
   float2 *T1 = reinterpret_cast<float2 *>(Tw + 512);  // w_n^t2, t2 < 1024 (pass A's column twiddle)
   uint64_t *full = reinterpret_cast<uint64_t *>(T1 + 1024);
   const int64_t tiles = (a.pulses + PPT - 1) / PPT;
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
   for (int i = tid; i < 512; i += kWs3T) Tw[i] = reinterpret_cast<const float4 *>(a.tw)[i];
   for (int i = tid; i < 1024; i += kWs3T) T1[i] = twn((uint32_t)i, log2n);
   if constexpr (PAD > 0) {  // the margins are never written again
-    for (int i = tid; i < 3 * PPT * 2 * PAD; i += kWs3T) {
+    for (int i = tid; i < NSLOT * PPT * 2 * PAD; i += kWs3T) {
       const int sl = i / (PPT * 2 * PAD), j = i - sl * (PPT * 2 * PAD), pl = j / (2 * PAD), e = j - pl * 2 * PAD;
       slots[sl * SLOT + pl * PS + (e < PAD ? e : n + e)] = make_float2(0.f, 0.f);
     }
@@ -97,31 +99,32 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
     const int np = (int)min((int64_t)PPT, a.pulses - p0);
     const unsigned bytes = (unsigned)(np * n * sizeof(float2));
     fence_proxy_async();
-    mbar_arrive_expect_tx(&full[i % 3], bytes);
+    mbar_arrive_expect_tx(&full[i % NSLOT], bytes);
     if constexpr (PAD == 0) {
-      bulk_load(slots + (i % 3) * SLOT, a.src + p0 * (int64_t)n, bytes, &full[i % 3]);
+      bulk_load(slots + (i % NSLOT) * SLOT, a.src + p0 * (int64_t)n, bytes, &full[i % NSLOT]);
     } else {
       for (int pl = 0; pl < np; ++pl)
-        bulk_load(slots + (i % 3) * SLOT + pl * PS + PAD, a.src + (p0 + pl) * (int64_t)n, n * sizeof(float2), &full[i % 3]);
+        bulk_load(slots + (i % NSLOT) * SLOT + pl * PS + PAD, a.src + (p0 + pl) * (int64_t)n, n * sizeof(float2),
+                  &full[i % NSLOT]);
     }
   };
   if (tid == 0) {
-    for (int s = 0; s < 3; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
-    for (int64_t i = 0; i < 3; ++i)
+    for (int64_t i = 0; i < NSLOT; ++i)
       if (tile_of(i) < tiles) stage(i);
   }
   __syncthreads();
-  auto group_sync = [grp] { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(kWs3GT) : "memory"); };
+  auto group_sync = [grp] { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(GT) : "memory"); };
 
-  for (int64_t i = grp; tile_of(i) < tiles; i += 2) {
-    float2 *sb = slots + (i % 3) * SLOT;
-    mbar_wait(&full[i % 3], (unsigned)((i / 3) & 1));
+  for (int64_t i = grp; tile_of(i) < tiles; i += NGRP) {
+    float2 *sb = slots + (i % NSLOT) * SLOT;
+    mbar_wait(&full[i % NSLOT], (unsigned)((i / NSLOT) & 1));
     const int64_t p0 = tile_of(i) * PPT;
     const int np = (int)min((int64_t)PPT, a.pulses - p0);
     // ---- A: columns (pulse pl, t2), forward N1-point DFT, x w_n^(k1 t2) / n
 #pragma unroll 1
-    for (int c = gtid; c < np * 1024; c += kWs3GT) {
+    for (int c = gtid; c < np * 1024; c += GT) {
       float2 *col = sb + (c >> 10) * PS + PAD + (c & 1023);
       const uint32_t t2 = (uint32_t)(c & 1023);
       float2 v[N1];
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
     group_sync();
     // ---- B: rows (pulse pl, k1): forward DFT -> phase -> inverse DFT -> x conj w_n^(k1 t2)
 #pragma unroll 1
-    for (int rw = warp; rw < np * N1; rw += kWs3GW) {
+    for (int rw = warp; rw < np * N1; rw += GW) {
       const int pl = rw / N1, k1 = rw - pl * N1;
       float2 *row = sb + pl * PS + PAD + 1024 * k1;
       float2 v[32];
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
     group_sync();
     // ---- C: columns, inverse N1-point DFT over k1 -> y[1024 t1 + t2]
 #pragma unroll 1
-    for (int c = gtid; c < np * 1024; c += kWs3GT) {
+    for (int c = gtid; c < np * 1024; c += GT) {
       const int pl = c >> 10;
       float2 *col = sb + pl * PS + PAD + (c & 1023);
       float2 v[N1];
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
       constexpr int R = dop_r(DOPW), SEG = 32 * R, NSEG = (n + SEG - 1) / SEG;
       group_sync();
 #pragma unroll 1
-      for (int q = warp; q < np * NSEG; q += kWs3GW) {
+      for (int q = warp; q < np * NSEG; q += GW) {
         const int pl = q / NSEG, sg = q - pl * NSEG;
         DopTile cur;
         cur.pulse = p0 + pl;
@@ -222,8 +225,8 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
         dop_tile_compute<DSECOND, DOPW, 0, R, true>(sb + pl * PS, cur, DOPW, nullptr, y, n, carrier);
       }
     }
-    group_sync();  // slot drained: stream tile i + 3 into it
-    if (gtid == 0 && tile_of(i + 3) < tiles) stage(i + 3);
+    group_sync();  // slot drained: stream tile i + NSLOT into it
+    if (gtid == 0 && tile_of(i + NSLOT) < tiles) stage(i + NSLOT);
   }
 }
 

@@ -53,7 +53,7 @@ def near_dc_tones(n, fs, seed, kmax=8):
 
 # ----------------------------------------------------------------------------- huge |nu| (near-DC bins)
 @pytest.mark.parametrize("fs", [2.048e9, 204.8e6, 51.2e6])
-@pytest.mark.parametrize("log2n", [7, 8, 9, 10, 11, 12, 13, 16, 20, 21, 22])
+@pytest.mark.parametrize("log2n", [7, 8, 9, 10, 11, 12, 13, 14, 16, 20, 21, 22])
 def test_iono_near_dc_huge_nu_vs_oracle(dc, fs, log2n):
     # fc = 0, TEC = 2e18: bin 1 of a 2^21 pulse at 51.2 MHz is f = 24 Hz, nu = 2.2e10 cycles.  The
     # model is meaningless there (valid for f >> 6 MHz) but the ABI accepts it and the oracle
@@ -215,10 +215,10 @@ def test_doppler_kaiser_alpha_one_bit_exact_all_shapes(dc, kb):
 
 
 # ----------------------------------------------------------------------------- in-CTA four-step, many tiles
-@pytest.mark.parametrize("log2n", [11, 12, 13])
+@pytest.mark.parametrize("log2n", [11, 12, 13, 14])
 def test_iono_incta_fourstep_many_tiles_sampled(dc, log2n):
-    # n = 2^11 .. 2^13 run on the in-CTA four-step kernel (wsmall.cuh): 8192-sample tiles cycling through
-    # three staging slots and two warp groups per CTA.  1187 pulses give every CTA several trips round the
+    # n = 2^11 .. 2^14 run on the in-CTA four-step kernel (wsmall.cuh): 8192-sample tiles cycling through
+    # three staging slots and two warp groups per CTA (2^14: one pulse per tile, one slot, one group).  1187 pulses give every CTA several trips round the
     # slot ring plus a ragged last tile; sampled pulses (including the last) against the oracle,
     # element-wise, and the forward model (Eq. 14) on the same train
     import torch

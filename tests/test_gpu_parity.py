@@ -567,11 +567,11 @@ def test_correct_c3_physics_dilated_dispersed_echo(dc):
 
 
 # ----------------------------------------------------------------------------- fused single-round-trip dc_correct (NEXT-1)
-@pytest.mark.parametrize("log2n", [10, 11, 12, 13])
+@pytest.mark.parametrize("log2n", [10, 11, 12, 13, 14])
 @pytest.mark.parametrize("W", [16, 32])
 @pytest.mark.parametrize("case", ["fast1", "second"])
 def test_correct_fused_small_vs_oracle(dc, log2n, W, case):
-    # n = 2^11 .. 2^13 with W = 16 / 32 and a first/second-order alpha run iono + Doppler in ONE kernel
+    # n = 2^10 .. 2^14 with W = 16 / 32 and a first/second-order alpha run iono + Doppler in ONE kernel
     # (the ionospheric result stays in shared memory); parity with the oracle's Doppler(iono(x))
     import torch
     n = 1 << log2n

@@ -45,6 +45,6 @@ def rate(log2n, total_log2=28, reps=5, what="iono"):
 for l in [int(a) for a in os.environ.get("KB_IONO_N", "8,10,12,13,14,16,18,20,22,24").split(",")]:
     out[f"iono_2e{l}"] = rate(l)
 out["correct_2e20"] = rate(20, what="correct")
-for l in (10, 11, 12, 13):  # the fused single-round-trip dc_correct (n = 2^11 .. 2^13, W = 32)
+for l in (10, 11, 12, 13, 14):  # the fused single-round-trip dc_correct (n = 2^10 .. 2^14, W = 32)
     out[f"correct_2e{l}"] = rate(l, what="correct")
 print(json.dumps(out), flush=True)
