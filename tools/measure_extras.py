@@ -195,7 +195,7 @@ def iono_sweep():
         sps = batch * n / (ms / 1e3)
         inf = p.info()
         rows.append({"n": n, "batch": batch, "ms": ms, "samples_per_s": sps, "frac_hbm": 16 * sps / (hbm * 1e9),
-                     "hbm_round_trips": 1 if inf["regime"] == 0 else 3})
+                     "hbm_round_trips": 1 if (inf["regime"] == 0 or n == 1 << 14) else 3})
         p.close()
         del xs
         torch.cuda.empty_cache()
