@@ -176,6 +176,9 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
   const int sms = ls.sms, per_sm = ls.per_sm;
   int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
+#ifdef DC_DOP_GRID_CAP
+  grid = std::min<int64_t>(grid, DC_DOP_GRID_CAP);  // tuning builds only
+#endif
   grid = std::min<int64_t>(grid, kDopMaxCtas);
   static_assert(kDopBufs <= 4 && sizeof(DopTile) == 48, "kDopDescBytes sizing");
   CUtensorMap dmap;  // the per-CTA geometry slots: {6 x 8 bytes, slot}, one 48-byte box per tile
@@ -193,8 +196,12 @@ static cudaError_t launch_pipe(const DopplerArgs &a) {
 // T = 128 187.5 / 169.2 GS/s): short pulses (n < 2^16, a few tiles per pulse) take 128-thread CTAs (4 per
 // SM: finer tiles, less quantisation); long pulses 512 (one 16-warp CTA per SM: one set of staging buffers
 // and fewer, longer tiles), except W <= 16 (256: 303 vs 286 GS/s) and the tapered windows (256).
+#ifndef DC_DOP_FORCE_T
+#define DC_DOP_FORCE_T 0  // tuning builds only: force the CTA size (128 / 256 / 512)
+#endif
 template <bool SECOND, int WT, int TAPER>
 static cudaError_t launch_pipe_t(const DopplerArgs &a) {
+  if constexpr (DC_DOP_FORCE_T > 0) return launch_pipe<SECOND, WT, TAPER, DC_DOP_FORCE_T>(a);
   if constexpr (TAPER == 0) {
     if (a.n < (1 << 16)) return launch_pipe<SECOND, WT, TAPER, 128>(a);
     if constexpr (WT == 0 || WT > 16) {
