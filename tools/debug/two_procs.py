@@ -19,8 +19,11 @@ def work(rank, mode, lib, port, q, what):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=2)
     torch.cuda.set_device(0)
+    npul = 512
+    if "x" in what:  # e.g. correct20x256: 256 pulses per process
+        what, npul = what.split("x")[0], int(what.split("x")[1])
     log2n = int(what[-2:])
-    n, pulses = 1 << log2n, 512 * (1 << 20) // (1 << log2n)
+    n, pulses = 1 << log2n, npul * (1 << 20) // (1 << log2n)
     bank = synth.waveform_bank(n, count=16)
     idx = (np.arange(pulses) + pulses * rank) % 16
     x = torch.from_numpy(bank[idx]).cuda()
@@ -32,6 +35,9 @@ def work(rank, mode, lib, port, q, what):
         for _ in range(6):
             if what.startswith("correct"):
                 p.correct(x, y, tec, alpha)
+            elif what.startswith("seq"):  # the two stages as separate calls on the user's buffers
+                p.iono(x, tec)
+                p.doppler(x, y, alpha)
             elif what.startswith("iono"):
                 p.iono(x, tec)
             elif what.startswith("pq"):
