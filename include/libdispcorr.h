@@ -78,8 +78,8 @@ dc_status dc_sync(dc_plan_t plan);
  *   X = DFT(x) (forward kernel e^{-i 2 pi k t / n});  X_k *= exp(-i 2 pi nu_k) / n with
  *   nu_k = 2 K2 / (c f_k), K2 = dc_k2_per_tec() * tec[p]  (two-way), nu_k = 0 if f_k <= 0
  *   (reading R3); x = IDFT(X).  tec: host double[batch], el/m^2, each finite and >= 0.
- * batch >= 1.  One HBM round trip per pulse for n <= 8192; n > 8192 uses a three-pass
- * four-step decomposition in place on x. */
+ * batch >= 1.  One HBM round trip per pulse for n <= 2^14 (n = 2^14: the in-CTA four-step kernel of
+ * regime 1); n > 2^14 uses a three-pass four-step decomposition in place on x. */
 dc_status dc_iono(dc_plan_t plan, void *x, int64_t batch, const double *tec);
 
 /* Forward ionospheric model, Eq. 14: the same with exp(+i 2 pi nu_k).
@@ -149,7 +149,7 @@ dc_status dc_set_window(dc_plan_t plan, int kind, double param);
  * result in y (must not overlap x).  Pulses run in launch groups of <= 2 GiB; the
  * ionospheric result of a group is kept in a plan-owned device buffer (allocated on the
  * first call, sized to min(batch, group)) between the stages -- except for single-CTA pulses
- * (n = 2^10 .. 2^13) with W = 16 or 32, the rectangular window and |1/alpha - 1| within the
+ * (n = 2^10 .. 2^14) with W = 16 or 32, the rectangular window and |1/alpha - 1| within the
  * first/second-order range, where one fused kernel reads x and writes y once (16 B/sample). */
 dc_status dc_correct(dc_plan_t plan, const void *x, void *y, int64_t batch, const double *tec,
                      const double *alpha);
@@ -165,7 +165,7 @@ typedef struct {
   int64_t n;             /* samples per pulse */
   int log2n;
   int taps;              /* sinc window W */
-  int regime;            /* 0 = single-CTA fused FFT (n <= 8192), 1 = three-pass four-step */
+  int regime;            /* 0 = single-CTA fused FFT (n <= 8192), 1 = four-step (n = 2^14: in one CTA, one HBM round trip) */
   int64_t n1, n2;        /* four-step split n = n1 * n2 (t = n2 t1 + t2, k = k1 + n1 k2); 0 if regime 0 */
   int64_t chunk_pulses;  /* pulses per dc_correct chunk (scratch = chunk_pulses * n * 8 bytes) */
   int64_t scratch_bytes; /* device scratch owned by the plan */
@@ -178,9 +178,9 @@ dc_status dc_plan_info(dc_plan_t plan, dc_plan_info_t *info);
  * the plan launches is bracketed by CUDA events on the plan's stream; dc_profile_read()
  * synchronises the stream and returns, per class, the launches, summed device milliseconds and
  * samples processed since the last reset.  Classes: DC_K_IONO_SMALL (regime-0 fused FFT ->
- * phase -> IFFT), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler),
+ * phase -> IFFT; also n = 2^14's in-CTA four-step), DC_K_FOURSTEP_A/B/C (regime-1 passes), DC_K_DOPPLER (sinc resampler),
  * DC_K_PQ (one record per dc_doppler_pq launch group: all of its kernels), DC_K_CORRECT_FUSED (the
- * single-round-trip dc_correct kernel of short pulses: n = 2^10 .. 2^13, W = 16 or 32, no taper). */
+ * single-round-trip dc_correct kernel of short pulses: n = 2^10 .. 2^14, W = 16 or 32, no taper). */
 enum { DC_K_IONO_SMALL = 0, DC_K_FOURSTEP_A = 1, DC_K_FOURSTEP_B = 2, DC_K_FOURSTEP_C = 3, DC_K_DOPPLER = 4,
        DC_K_PQ = 5, DC_K_CORRECT_FUSED = 6, DC_K_CLASSES = 7 };
 typedef struct {
