@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(T, 65536 / (T * 128))
                         int buf_elems, const __grid_constant__ TaperCoef tc, DopTile *__restrict__ gdesc,
                         const __grid_constant__ CUtensorMap dmap) {
   pdl_wait();  // programmatic dependent launch (dc_common.cuh); the trigger is implicit at exit
-  constexpr int R = dop_r(WT), M = T * R, SEG = 32 * R;
+  constexpr int R = dop_r_pipe(WT, T), M = T * R, SEG = 32 * R;
   extern __shared__ __align__(1024) float4 xs4[];
   float2 *xs = reinterpret_cast<float2 *>(xs4);                     // kDopBufs x buf_elems input spans
   float2 *ob = xs + kDopBufs * buf_elems;                            // M output staging (per warp)
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) doppler_exact_kernel(const float2 *__rest
 
 template <bool SECOND, int WT, int TAPER, int T>
 static cudaError_t launch_pipe(const DopplerArgs &a) {
-  constexpr int R = dop_r(WT), M = T * R;
+  constexpr int R = dop_r_pipe(WT, T), M = T * R;
   const int64_t tiles = (a.n + M - 1) / M * a.pulses;
   // staged span <= M * max(beta) + W + R + 6 samples (fast path: |beta - 1| <= 4.4e-4)
   const int span = (int)(M * (1.0 + kDopMaxDrift)) + a.taps + R + 16;
@@ -247,16 +247,22 @@ static cudaError_t launch_doppler_exact(const DopplerArgs &a) {
 }
 
 // Path choice from the largest |beta - 1| among the launched pulses (host-known):
-//   drift = |beta - 1| * R / 2 is the largest Taylor step delta of the fast kernel.
-//   first order  if drift <= 2e-4 (truncation <= 1.64 delta^2 <= 7e-8 per tap weight)
+//   drift = |beta - 1| * (R + 1) / 2 is the largest Taylor step delta of the fast kernels (R = 13, the
+//   largest R any of them uses for W <= 32, so the choice holds for every kernel that may run).
+//   first order  if drift <= 5e-4 (truncation delta^2 / 2 |w''| <= 4.1e-7 per tap weight; summed over the
+//                window's sum |w''| ~ 25 it stays below 1e-6 of the output rms -- round 2 raised the
+//                bound from 2e-4, which sent the C4 train's largest |v| ~ 5 km/s to the second order)
 //   second order if drift <= 2e-3 (truncation <= 1.3 delta^3 <= 1.1e-8)
 //   exact taps otherwise.
 // The tapered weights have the first-order path only (h'' of sinc K is not formed): second-order
 // drifts take the exact path.
 int doppler_path(double max_abs_beta_m1, bool taper, int W) {
-  const int R = (W == 128) ? dop_r(128) : kDopR;  // the fast kernel's R for this W (compile-time W only)
+  const int R = (W == 128) ? dop_r(128) : (W == 64 ? kDopR : 13);  // the largest R of the kernels for this W
   const double drift = max_abs_beta_m1 * (R / 2 + 0.5);
-  if (drift <= 2.0e-4) return 1;
+#ifndef DC_DOP_FAST1
+#define DC_DOP_FAST1 5.0e-4
+#endif
+  if (drift <= DC_DOP_FAST1) return 1;
   if (drift <= kDopMaxDrift && !taper) return 2;
   return 0;
 }

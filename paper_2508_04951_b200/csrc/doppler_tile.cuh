@@ -19,6 +19,12 @@ constexpr int kDopR = DC_DOP_R;  // outputs per thread: odd, so lanes' windows (
 // R per compile-time W: R = 9 at W = 128 (the 129-tap loop of R = 11 is register-bound: 58 vs 45 GS/s
 // measured), 11 otherwise (W = 32: 201 vs 190 GS/s for R = 9, 146 for R = 13)
 __host__ __device__ constexpr int dop_r(int WT) { return WT >= 128 ? 9 : kDopR; }
+// R of doppler_pipe_kernel<.., T>: 13 for the compile-time W <= 32 at T >= 256 (round 2, on the first-order
+// path: W = 32 204.7 vs 199.5 GS/s, W = 16 320 vs 304, Kaiser-8 103 vs 96); T = 128 (n < 2^16) keeps 11
+// (4096-sample pulses: 169 vs 146 -- tile quantisation), W = 64 keeps 11 (111.6 vs 109.5), W = 128 keeps 9
+__host__ __device__ constexpr int dop_r_pipe(int WT, int T) {
+  return WT >= 128 ? 9 : (T >= 256 && WT > 0 && WT <= 32) ? 13 : kDopR;
+}
 constexpr int kDopM = kDopT * kDopR;     // outputs per tile (R = kDopR)
 constexpr int kDopSeg = 32 * kDopR;      // outputs per warp (even: 16-byte aligned bulk stores)
 constexpr double kDopMaxDrift = 2.0e-3;  // max |beta - 1| * R / 2 for the fast path

@@ -646,3 +646,32 @@ def test_doppler_hann_full_size_sampled(dc):
     for i, a in enumerate(alphas):
         ref = O.doppler_at(x[i].astype(np.complex128), 32, 2.048e9, 0.0, a, idx, kaiser=O.HANN)
         assert rel_l2(y[i][idx], ref).max() < TOL
+
+
+# ----------------------------------------------------------------------------- long-pulse Doppler kernels (R = 13)
+# n >= 2^16 runs doppler_pipe_kernel at 256 / 512 threads with R = 13 outputs per thread for W <= 32; the
+# first-order path holds up to drift |beta - 1| (R + 1) / 2 = 5e-4 (|beta - 1| ~ 7.1e-5): "edge" sits just
+# inside it, "fast2" on the second-order path
+LONG_ALPHAS = {
+    "fast1": [1 + 3.3e-5, 1 - 3.3e-5, 1.0],
+    "edge": [1 + 7.0e-5, 1 - 7.1e-5, 1 + 2e-6],
+    "fast2": [1 + 2.5e-4, 1 - 2.0e-4, 1 + 1e-4],
+}
+
+
+@pytest.mark.parametrize("case", list(LONG_ALPHAS))
+@pytest.mark.parametrize("W", [8, 16, 25, 32, 64])
+def test_doppler_long_pulse_kernels_vs_oracle(dc, case, W):
+    n = 1 << 16
+    alphas = np.array(LONG_ALPHAS[case])
+    x = synth.complex_gaussian(n, seed=W + 31, batch=len(alphas)).astype(np.complex64)
+    for fs, fc in ((2.048e9, 0.0), (51.2e6, 422e6)):
+        y = gpu_doppler(dc, x, W, fs, fc, alphas)
+        ref = O.run_batch("doppler", x, fs, fc, W, None, alphas)
+        assert rel_l2(y, ref).max() < TOL, (case, W, fs, fc, rel_l2(y, ref).max())
+        if case == "fast1":
+            assert np.array_equal(y[2], x[2])  # alpha = 1 bit-exact on the R = 13 kernels too
+    if case != "fast2":  # tapered: first-order path only
+        y = gpu_doppler_taper(dc, x, W, 2.048e9, 0.0, alphas, 8.0)
+        ref = O.run_batch("doppler", x, 2.048e9, 0.0, W, None, alphas, kaiser=8.0)
+        assert rel_l2(y, ref).max() < TOL, (case, W, "kaiser", rel_l2(y, ref).max())
