@@ -67,6 +67,9 @@ __global__ void __launch_bounds__(T, 65536 / (T * 128))
     const int b = (int)(i % kDopBufs);
     const uint32_t it = blockIdx.x + i * gridDim.x;
     const DopTile t = dop_tile<R, T>(it, tiles_per_pulse, W, pp[pulse_base + dop_pulse(it, tiles_per_pulse)].beta);
+#ifdef DC_DEBUG_CHECKS
+    if (dop_nbox(t) * kDopBox > buf_elems) __trap();  // the staged span fits its buffer
+#endif
     const int slot = (int)blockIdx.x * kDopBufs + b;
     dop_stage_tma(xs + b * buf_elems, t, &xmap, &full[b], dslot(b), gdesc + slot, &dmap, slot);
   };

@@ -175,6 +175,10 @@ __device__ __forceinline__ void dop_tile_compute(const float2 *__restrict__ sb, 
   const double md = (double)mt;
   const double x0 = __dsub_rn(__dmul_rn(md, beta), halfW);
   const int64_t B = (int64_t)floor(x0) + 1 - lo_shift;  // union base: x[B + i], i = 0 .. W + R - 1
+#ifdef DC_DEBUG_CHECKS
+  // debug builds (tests/test_gpu_debug_checks.py): the union window lies inside the staged / resident span
+  if (mt < n && (B - cur.Bcta < 0 || B - cur.Bcta + W + R > cur.span)) __trap();
+#endif
   const double Bd = (double)B;
   const uint32_t own1 = dop_membership<R>(md, beta, halfW, Bd, x0);
   // Taylor steps delta_r = (r - R/2)(beta - 1): pairs for FFMA2 (+ one single for odd R)

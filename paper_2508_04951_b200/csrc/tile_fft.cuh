@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(TileCfg<P, LOGE, NB, ROW, MODE>::T, 1) tile_ff
         cur.pulse = p;
         cur.Bcta = -kCsPad;
         cur.beta = a.pp[a.pulse_base + p].beta;
-        cur.span = 0;
+        cur.span = CFG::DSTRIDE;  // the zero-margined pulse
         cur.pad0 = 0;
         cur.pad1 = 0;
         for (int m0 = 0; m0 < L; m0 += T * kDopR) {

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kWcNW * 32, 1) warp_correct1024_kernel(const W
     cur.pulse = it;
     cur.Bcta = -kCsPad;
     cur.beta = pr.beta;
-    cur.span = 0;
+    cur.span = kWcD;  // the zero-margined pulse: x[k] at wk[kCsPad + k]
     cur.pad0 = 0;
     cur.pad1 = 0;
 #pragma unroll 1

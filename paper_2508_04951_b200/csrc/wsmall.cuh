@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kWs3T, 1) warp_small3_kernel(const WarpArgs a,
         cur.m0 = (int64_t)sg * SEG - (int64_t)(tid >> 5) * SEG;
         cur.Bcta = -PAD;
         cur.beta = a.pp[a.pulse_base + p0 + pl].beta;
-        cur.span = 0;
+        cur.span = PS;  // the zero-margined pulse: x[k] at slot[pl PS + PAD + k]
         cur.pad0 = 0;
         cur.pad1 = 0;
         dop_tile_compute<DSECOND, DOPW, 0, R, true>(sb + pl * PS, cur, DOPW, nullptr, y, n, carrier);

@@ -14,17 +14,23 @@ from paper_2508_04951_b200 import build as b  # noqa: E402
 
 
 def build_variant(src: str, name: str, flags: list[str]) -> str:
+    """src: one csrc/*.cu file, or several joined by '+' (each recompiled with the flags)."""
     vdir = os.path.join(b.LIB_DIR, "variants")
     os.makedirs(vdir, exist_ok=True)
-    obj = os.path.join(vdir, f"{name}_{src}.o")
-    r = subprocess.run(["nvcc", *b.NVCC_FLAGS, *flags, "-Xptxas", "-v", "-c", os.path.join(b.SRC_DIR, src), "-o", obj],
-                       capture_output=True, text=True)
-    if r.returncode:
-        raise RuntimeError(r.stderr[-3000:])
-    spill = sorted({ln.strip() for ln in r.stderr.splitlines() if "spill stores" in ln and " 0 bytes spill" not in ln})
-    objs = [os.path.join(b.LIB_DIR, "obj", os.path.basename(s) + ".o") for s in b.sources() if os.path.basename(s) != src]
+    srcs = src.split("+")
+    vobjs, spill = [], set()
+    for sname in srcs:
+        obj = os.path.join(vdir, f"{name}_{sname}.o")
+        r = subprocess.run(["nvcc", *b.NVCC_FLAGS, *flags, "-Xptxas", "-v", "-c", os.path.join(b.SRC_DIR, sname), "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode:
+            raise RuntimeError(r.stderr[-3000:])
+        spill |= {ln.strip() for ln in r.stderr.splitlines() if "spill stores" in ln and " 0 bytes spill" not in ln}
+        vobjs.append(obj)
+    spill = sorted(spill)
+    objs = [os.path.join(b.LIB_DIR, "obj", os.path.basename(s) + ".o") for s in b.sources() if os.path.basename(s) not in srcs]
     lib = os.path.join(vdir, f"{name}.so")
-    subprocess.check_call(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, obj, *objs,
+    subprocess.check_call(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *vobjs, *objs,
                            "-Xlinker", "--version-script=" + os.path.join(b.SRC_DIR, "exports.map")])
     return f"{lib}  spills: {len(spill)} kernels" + ("" if not spill else f" (max {max(spill)})")
 
